@@ -1,0 +1,204 @@
+/*
+ * pi.h -- C ABI of libpi: PowerInfer's predictor-gated, neuron-aware sparse FFN
+ * (arXiv 2312.12456) for batch-1 / small-batch decoding, hand-written for sm_100a.
+ *
+ * Citations: "P:n" = line n of the paper text, "S:n" = line n of
+ * SPEC.md.  Readings Rk of ambiguous passages are listed in DESIGN.md.
+ *
+ * One layer, one call sequence per decode step:
+ *   pi_predict     a1+a2  predictor MLP + threshold -> per-token neuron bitmask
+ *   pi_compact     a3     ascending ids of neurons active for any token (union)
+ *   pi_sparse_ffn  a4+a5  row-sparse up(/gate) GEMV + column-sparse down GEMV
+ *   pi_layer_forward      all of the above in one persistent kernel
+ *   pi_partition          host-side neuron -> GPU placement (adapted)
+ *
+ * Conventions shared by every entry point
+ *   - Every call returns pi_status; nothing throws across the ABI.  On error a
+ *     message is available from pi_last_error() (thread-local, valid until the
+ *     next pi_* call on that thread).
+ *   - Host-side validation runs before anything is enqueued.  On a validation
+ *     error nothing is enqueued and outputs are untouched.  Asynchronous device
+ *     faults surface as PI_ERR_CUDA at a later call.
+ *   - "dev" pointers are CUDA device pointers, "host" pointers are host memory.
+ *   - Device calls are asynchronous on `stream`, never synchronise the host
+ *     (except the *_host variants), and are CUDA-graph capturable.  The active
+ *     count stays on the device; kernels are sized for the worst case.
+ *   - A layer handle owns workspace: at most one call in flight per handle
+ *     (SPEC likewise serialises infer calls).
+ *   - Activations x, g, z, h, y are fp32 ("intermediate activations in FP32",
+ *     P:854-855); weights are fp16 (the paper's) or bf16.
+ *   - Mask layout: uint32 words [B, ceil(m_local/32)], bit (i & 31) of word
+ *     (i >> 5) = local neuron i, token-major.
+ */
+#ifndef PI_H_
+#define PI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *pi_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+typedef struct pi_layer pi_layer;        /* opaque layer handle */
+
+typedef enum {
+  PI_OK = 0,
+  PI_ERR_INVALID_ARGUMENT = 1, /* NULL handle/pointer, batch < 1 or > max_batch, bad enum     */
+  PI_ERR_SHAPE = 2,            /* inconsistent dims; message names layer_id and expected/actual */
+  PI_ERR_INDEX = 3,            /* neuron id out of range / not strictly ascending */
+  PI_ERR_ALIGNMENT = 4,        /* device pointer not 16-B aligned, d % 8 != 0, rank % 8 != 0  */
+  PI_ERR_UNSUPPORTED = 5,      /* dtype/act combination not compiled, device is not sm_100     */
+  PI_ERR_CUDA = 6,             /* CUDA error; message carries cudaGetErrorString               */
+  PI_ERR_OUT_OF_MEMORY = 7
+} pi_status;
+
+typedef enum { PI_DT_F16 = 0, PI_DT_BF16 = 1 } pi_dtype;
+/* PI_ACT_RELU: h = relu(a).  PI_ACT_REGLU: h = relu(W_gate[i].x) * a (reading R5). */
+typedef enum { PI_ACT_RELU = 0, PI_ACT_REGLU = 1 } pi_act;
+/* predictor hidden non-linearity (P:555 names only "a single hidden" layer; reading R1) */
+typedef enum { PI_PRED_RELU = 0, PI_PRED_LINEAR = 1 } pi_pred_act;
+
+/* PI_FLAG_INPUT_RMSNORM: predictor and FFN both use x_hat = x * rsqrt(mean(x^2) + 1e-6)
+ * per token (harness stand-in for the pre-FFN norm of chained stacks; reading R19). */
+#define PI_FLAG_INPUT_RMSNORM 1u
+
+#define PI_MAX_BATCH 8
+
+/* Layer description.  Weight pointers are DEVICE pointers in the PyTorch
+ * nn.Linear layouts of the GLOBAL layer (m_total neurons); the handle keeps the
+ * rows named by neuron_ids ("neuron tables ... correlate each neuron to its
+ * original position in the matrix"). */
+typedef struct {
+  int32_t layer_id;          /* used in messages only                                          */
+  int32_t d;                 /* hidden size; d % 8 == 0                                         */
+  int32_t m_total;           /* FFN width of the global layer                                   */
+  int32_t rank;              /* predictor hidden width r; r % 8 == 0                */
+  int32_t m_local;           /* neurons owned by this handle (= m_total when unsharded)         */
+  const int32_t *neuron_ids; /* host [m_local], strictly ascending global ids; NULL = 0..m_total-1 */
+  pi_dtype dtype;
+  pi_act act;
+  pi_pred_act pred_act;
+  const void *w_up;   /* dev [m_total, d]  FC1: row i = neuron i (P:107 footnote)           */
+  const void *w_gate; /* dev [m_total, d]  required iff act == PI_ACT_REGLU                */
+  const void *w_down; /* dev [d, m_total]  FC2 (nn.Linear fc2.weight): column i = neuron i */
+  const void *b_up;   /* dev [m_total] or NULL; added before the activation          */
+  const void *b_down; /* dev [d] or NULL; give it to exactly ONE shard (merge adds it once) */
+  const void *p_w1;   /* dev [rank, d]     predictor input->hidden, replicated on shards   */
+  const void *p_b1;   /* dev [rank] or NULL                                                 */
+  const void *p_w2;   /* dev [m_total, rank] predictor hidden->output                      */
+  const void *p_b2;   /* dev [m_total] or NULL                                              */
+  float logit_threshold; /* neuron active iff logit z > t; t = 0 <=> sigmoid(z) > 0.5 (S:216,
+                            reading R3); -INFINITY => all finite logits; NaN logits inactive */
+  int32_t max_batch;     /* 1..PI_MAX_BATCH; sizes the workspace                               */
+  uint32_t flags;        /* PI_FLAG_*                                                          */
+} pi_layer_desc;
+
+typedef struct {
+  int32_t d, m_local, rank, max_batch, mask_words; /* mask_words = ceil(m_local/32) */
+  int32_t dtype, act, pred_act;
+  uint32_t flags;
+  int32_t num_sms;          /* SMs of the device the handle lives on                */
+  int64_t weight_bytes;     /* library-owned weight bytes on the device             */
+  int64_t workspace_bytes;  /* library-owned workspace bytes                        */
+  int32_t launches_per_forward; /* kernel launches one pi_layer_forward call makes   */
+} pi_layer_info;
+
+/* Library version string, e.g. "libpi 0.1.0 sm_100a". */
+const char *pi_version(void);
+/* Thread-local message for the last failed call on this thread ("" if none). */
+const char *pi_last_error(void);
+
+/* Create a layer handle on the current CUDA device.  COPIES and repacks this
+ * shard's weights into library-owned device memory asynchronously on `stream`:
+ * up rows (gate|up interleaved per neuron for ReGLU), down transposed to
+ * [m_local, d] so each neuron's down vector is contiguous, P2 rows, b_up, b2
+ * gathered by neuron_ids; P1, b1, b_down copied.  The caller may free its
+ * tensors once `stream` has completed.  Errors: INVALID_ARGUMENT, SHAPE, INDEX
+ * (neuron_ids not strictly ascending or >= m_total), ALIGNMENT, UNSUPPORTED,
+ * OUT_OF_MEMORY, CUDA.  On error *out is NULL and nothing leaks. */
+pi_status pi_layer_create(const pi_layer_desc *desc, pi_stream_t stream, pi_layer **out);
+/* Synchronises the device, then frees everything the handle owns.  NULL is a no-op. */
+pi_status pi_layer_destroy(pi_layer *L);
+pi_status pi_layer_get_info(const pi_layer *L, pi_layer_info *info);
+
+/* a1 + a2: the predictor.
+ *   u = P1 x_b + b1 ; g = act_p(u) ; z = P2 g + b2 ; bit_{b,i} = (z_i > t)
+ * x      dev fp32 [B, d], row-major, 16-B aligned
+ * mask   dev uint32 [B, mask_words] (written, bits past m_local are 0)
+ * logits dev fp32 [B, m_local] or NULL (written if given)
+ * Errors: INVALID_ARGUMENT (NULL, B out of 1..max_batch), ALIGNMENT, CUDA. */
+pi_status pi_predict(pi_layer *L, const float *x, int32_t B, uint32_t *mask, float *logits,
+                     pi_stream_t stream);
+
+/* a3: compaction.  ids = ascending local indices i whose bit is set for ANY of
+ * the B tokens (union, reading R9; canonical ascending order S:43-46).
+ * mask      dev uint32 [B, mask_words]
+ * ids       dev int32 [m_local] (first *n_active entries written)
+ * n_active  dev int32 scalar (written on the device; never read back by the library)
+ * Errors: INVALID_ARGUMENT, CUDA. */
+pi_status pi_compact(pi_layer *L, const uint32_t *mask, int32_t B, int32_t *ids,
+                     int32_t *n_active, pi_stream_t stream);
+
+/* a4 + a5: the neuron-aware FFN over the compacted ids.
+ *   for k < n_active, i = ids[k], token b:
+ *     a = W_up[i] . x_b + b_up[i]
+ *     h = relu(a)  |  relu(W_gate[i] . x_b) * a           (act)
+ *     h := 0 if token b's own bit for i is 0             (per-token semantics)
+ *   y_b = b_down + sum_k h_{b,k} W_down[:, i_k]          (fp32; fixed order, no float atomics)
+ * ids       dev int32 [>= n_active], strictly ascending, < m_local (as pi_compact writes)
+ * n_active  dev int32 scalar
+ * mask      dev uint32 [B, mask_words]; may be NULL iff B == 1 (then every id counts)
+ * y         dev fp32 [B, d]; overwritten with this shard's partial (+ b_down if owned)
+ * Empty id set: y = b_down or 0.
+ * Errors: INVALID_ARGUMENT, ALIGNMENT, CUDA. */
+pi_status pi_sparse_ffn(pi_layer *L, const float *x, int32_t B, const int32_t *ids,
+                        const int32_t *n_active, const uint32_t *mask, float *y,
+                        pi_stream_t stream);
+
+/* All of a1..a5 for one layer and B tokens: the whole hot path.  Equivalent to
+ * pi_predict -> pi_compact -> pi_sparse_ffn.  mask_out / ids_out / n_active_out
+ * are optional dev outputs (NULL = keep in workspace). */
+pi_status pi_layer_forward(pi_layer *L, const float *x, int32_t B, float *y, uint32_t *mask_out,
+                           int32_t *ids_out, int32_t *n_active_out, pi_stream_t stream);
+
+/* Same as pi_layer_forward with HOST buffers: x_host fp32 [B, d] is copied to
+ * the device, the layer runs, y_host fp32 [B, d] is copied back, and the call
+ * returns after `stream` has finished (end-to-end path).  Pinned host memory
+ * gives asynchronous copies; pageable memory works but is slower. */
+pi_status pi_layer_forward_host(pi_layer *L, const float *x_host, int32_t B, float *y_host,
+                                pi_stream_t stream);
+
+/* Chain n_layers layers for B tokens: x_{l+1} = y_l (stacked configs).  x and y
+ * are dev fp32 [B, d]; x is not modified (ping-pong buffers live in layer 0's
+ * workspace).  All layers must share d and satisfy B <= max_batch.
+ * n_active_out: dev int32 [n_layers] (each layer's union count) or NULL. */
+pi_status pi_stack_forward(pi_layer *const *layers, int32_t n_layers, const float *x, int32_t B,
+                           float *y, int32_t *n_active_out, pi_stream_t stream);
+
+/* pi_stack_forward with HOST buffers (end-to-end path): x_host fp32 [B, d] is
+ * copied in, the stack runs, y_host fp32 [B, d] is copied out; returns after
+ * `stream` has finished. */
+pi_status pi_stack_forward_host(pi_layer *const *layers, int32_t n_layers, const float *x_host,
+                                int32_t B, float *y_host, pi_stream_t stream);
+
+/* Neuron -> shard placement (host, deterministic).  Adapts the paper's ILP
+ * (Eqs. 2-8) to G identical GPUs (reading R15): every neuron on
+ * exactly one shard (Eq. 3), equal counts (Eq. 6 with equal capacities),
+ * balanced expected active mass sum f_i (impact v_i = f_i, Eq. 1).  Neurons
+ * are ordered by (-f_i, i), cut into runs of `granule` similar-impact neurons
+ * (P:809 uses 64), and runs are dealt longest-first to the least-loaded shard
+ * with room (ties: lowest shard).
+ * freq          host float [m], finite, >= 0
+ * owner         host int32 [m]   shard of neuron i
+ * shard_ids     host int32 [m]   each shard's ids ascending, shards concatenated in order
+ * shard_offsets host int32 [n_shards + 1]
+ * Errors: INVALID_ARGUMENT (NULL, n_shards < 1, granule < 1, NaN/negative freq),
+ *         SHAPE (m % (granule * n_shards) != 0). */
+pi_status pi_partition(const float *freq, int32_t m, int32_t n_shards, int32_t granule,
+                       int32_t *owner, int32_t *shard_ids, int32_t *shard_offsets);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PI_H_ */

@@ -1,0 +1,382 @@
+// kernels.cuh -- libpi's per-call sm_100a kernels (pi_predict, pi_compact, pi_sparse_ffn).
+//
+// Each kernel is one step of SURVEY.md 8(a); pi_layer_forward fuses them in
+// fused.cuh.  All activations are fp32; weights fp16/bf16 streamed with 128-bit
+// non-allocating loads; every reduction has a fixed order (no float atomics),
+// so results are bitwise reproducible run to run.
+#pragma once
+
+#include "common.cuh"
+
+namespace pi {
+
+constexpr float kRmsEps = 1e-6f;  // reading R19
+
+// ---------------------------------------------------------------------------
+// per-token input scale: s_b = rsqrt(mean(x_b^2) + eps)   (PI_FLAG_INPUT_RMSNORM)
+// grid = B blocks, 256 threads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_rms_scale(const float *__restrict__ x, int d,
+                                                    float *__restrict__ scale) {
+  const int b = blockIdx.x;
+  const float *xb = x + (int64_t)b * d;
+  float s = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float v = xb[j];
+    s = fmaf(v, v, s);
+  }
+  __shared__ float red[8];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    scale[b] = rsqrtf(t / (float)d + kRmsEps);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a1: g[b, j] = act_p(s_b * (P1[j] . x_b) + b1[j])
+// 256 threads = 8 warps; 4 warps split the d-axis of one row; 2 rows per block.
+// ---------------------------------------------------------------------------
+template <typename T, int B, bool PRED_RELU>
+__global__ void __launch_bounds__(256) k_predict1(const T *__restrict__ p1, const T *__restrict__ b1,
+                                                   const float *__restrict__ x,
+                                                   const float *__restrict__ scale, int r, int d,
+                                                   float *__restrict__ g) {
+  constexpr int KS = 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 2 + warp / KS;
+  const int part = warp % KS;
+  float acc[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) acc[b] = 0.f;
+  if (row < r) {
+    const int chunks = d >> 3;
+    const T *w = p1 + (int64_t)row * d;
+    int c = part * 32 + lane;
+#pragma unroll 4
+    for (; c < chunks; c += 32 * KS) {
+      const Pack8 pw = ld_stream(w + (int64_t)c * 8);
+      float wf[8];
+      WT<T>::unpack(pw, wf);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float xv[8];
+        ld_x8(x + (int64_t)b * d + c * 8, xv);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[b] = fmaf(wf[k], xv[k], acc[b]);
+      }
+    }
+  }
+  __shared__ float red[8][B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const float v = warp_sum(acc[b]);
+    if (lane == 0) red[warp][b] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * B) {
+    const int rr = threadIdx.x / B, b = threadIdx.x % B;
+    const int orow = blockIdx.x * 2 + rr;
+    if (orow < r) {
+      float u = 0.f;
+#pragma unroll
+      for (int p = 0; p < KS; ++p) u += red[rr * KS + p][b];
+      if (scale) u *= scale[b];
+      if (b1) u += WT<T>::to_float(b1, orow);
+      if (PRED_RELU) u = fmaxf(u, 0.f);
+      g[(int64_t)b * r + orow] = u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a2: z = P2 g + b2; bit = z > t; one warp per 32 neurons = one mask word.
+// Lane groups of LPR lanes share a row (LPR = power of two <= min(32, r/8)).
+// 128 threads = 4 words per block; g staged in shared memory.
+// ---------------------------------------------------------------------------
+template <typename T, int B>
+__global__ void __launch_bounds__(128) k_predict2(const T *__restrict__ p2, const T *__restrict__ b2,
+                                                   const float *__restrict__ g, float t, int m,
+                                                   int r, int words, uint32_t *__restrict__ mask,
+                                                   float *__restrict__ logits) {
+  extern __shared__ float smem[];
+  float *gs = smem;                       // [B][r]
+  float *zb = smem + B * r;               // [4 warps][B][32]
+  for (int i = threadIdx.x; i < B * r; i += blockDim.x) gs[i] = g[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int word = blockIdx.x * 4 + warp;
+  if (word >= words) return;
+  const int chunks = r >> 3;
+  int lpr = 1;
+  while (lpr * 2 <= chunks && lpr < 32) lpr *= 2;
+  const int rp = 32 / lpr;                // rows in flight per warp iteration
+  const int q = lane / lpr, sl = lane % lpr;
+  float *zw = zb + warp * B * 32;
+  for (int it = 0; it < 32 / rp; ++it) {
+    const int rin = it * rp + q;
+    const int i = word * 32 + rin;
+    float acc[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) acc[b] = 0.f;
+    if (i < m) {
+      const T *w = p2 + (int64_t)i * r;
+#pragma unroll 2
+      for (int c = sl; c < chunks; c += lpr) {
+        float wf[8];
+        WT<T>::unpack(ld_stream(w + c * 8), wf);
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const float *gb = gs + b * r + c * 8;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[b] = fmaf(wf[k], gb[k], acc[b]);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float v = acc[b];
+      for (int o = lpr >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (sl == 0) {
+        float z = __int_as_float(0x7fc00000);          // NaN: never active
+        if (i < m) z = v + (b2 ? WT<T>::to_float(b2, i) : 0.f);
+        zw[b * 32 + rin] = z;
+      }
+    }
+  }
+  __syncwarp();
+  const int i = word * 32 + lane;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const float z = zw[b * 32 + lane];
+    const uint32_t bits = __ballot_sync(0xffffffffu, z > t);
+    if (lane == 0) mask[(int64_t)b * words + word] = bits;
+    if (logits && i < m) logits[(int64_t)b * m + i] = z;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a3: compaction of the union mask into ascending ids (single CTA, 1024 threads).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ mask, int B, int words,
+                                                   int32_t *__restrict__ ids,
+                                                   int32_t *__restrict__ n_active) {
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (words + blockDim.x - 1) / blockDim.x;
+  const int w0 = min(words, tid * per), w1 = min(words, w0 + per);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) {
+    uint32_t u = 0;
+    for (int b = 0; b < B; ++b) u |= mask[(int64_t)b * words + w];
+    cnt += __popc(u);
+  }
+  // block exclusive scan of cnt
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0;
+    int iv = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, iv, o);
+      if (lane >= o) iv += t;
+    }
+    wsum[lane] = iv - v;                  // exclusive warp offsets
+  }
+  __syncthreads();
+  int off = wsum[warp] + incl - cnt;
+  for (int w = w0; w < w1; ++w) {
+    uint32_t u = 0;
+    for (int b = 0; b < B; ++b) u |= mask[(int64_t)b * words + w];
+    while (u) {
+      const int bit = __ffs(u) - 1;
+      ids[off++] = w * 32 + bit;
+      u &= u - 1;
+    }
+  }
+  if (tid == blockDim.x - 1) *n_active = off;
+}
+
+// ---------------------------------------------------------------------------
+// a4: row-sparse up(/gate) GEMV.  One warp per active neuron (grid-stride over
+// the device-side count).  ReGLU rows are interleaved [gate | up] (2d elements).
+// h[b, k] = masked activation, fp32.
+// ---------------------------------------------------------------------------
+template <typename T, int B, bool REGLU>
+__global__ void __launch_bounds__(256) k_up(const T *__restrict__ wup, const T *__restrict__ bup,
+                                             const float *__restrict__ x,
+                                             const float *__restrict__ scale,
+                                             const int32_t *__restrict__ ids,
+                                             const int32_t *__restrict__ n_active,
+                                             const uint32_t *__restrict__ mask, int words, int d,
+                                             float *__restrict__ h, int hstride) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tw = (gridDim.x * blockDim.x) >> 5;
+  const int n = *n_active;
+  const int chunks = d >> 3;
+  const int64_t rowlen = REGLU ? 2 * (int64_t)d : (int64_t)d;
+  for (int k = gw; k < n; k += tw) {
+    const int i = ids[k];
+    const T *row = wup + (int64_t)i * rowlen;
+    float au[B], ag[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) au[b] = ag[b] = 0.f;
+#pragma unroll 8
+    for (int c = lane; c < chunks; c += 32) {
+      float wu[8], wg[8];
+      if (REGLU) {
+        WT<T>::unpack(ld_stream(row + c * 8), wg);
+        WT<T>::unpack(ld_stream(row + d + c * 8), wu);
+      } else {
+        WT<T>::unpack(ld_stream(row + c * 8), wu);
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float xv[8];
+        ld_x8(x + (int64_t)b * d + c * 8, xv);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          au[b] = fmaf(wu[q], xv[q], au[b]);
+          if (REGLU) ag[b] = fmaf(wg[q], xv[q], ag[b]);
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      au[b] = warp_sum(au[b]);
+      if (REGLU) ag[b] = warp_sum(ag[b]);
+    }
+    if (lane < B) {
+      float a = 0.f, gt = 0.f;
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (b == lane) { a = au[b]; gt = ag[b]; }
+      const float s = scale ? scale[lane] : 1.f;
+      a = a * s + (bup ? WT<T>::to_float(bup, i) : 0.f);
+      float hv = REGLU ? fmaxf(gt * s, 0.f) * a : fmaxf(a, 0.f);
+      if (mask && !((mask[(int64_t)lane * words + (i >> 5)] >> (i & 31)) & 1u)) hv = 0.f;
+      h[(int64_t)lane * hstride + k] = hv;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a5: column-sparse down GEMV, y_b = b_down + sum_k h[b,k] Wd_T[ids[k], :].
+// Block (tile, split): 8 warps own a 256-column tile; split s walks compacted
+// positions [s n / S, (s+1) n / S).  Warps reduce in fixed order through shared
+// memory into partial[s]; the last block of each tile (integer ticket) sums the
+// S partials in order s = 0..S-1 and adds b_down.  Deterministic, no float atomics.
+// ---------------------------------------------------------------------------
+template <typename T, int B>
+__global__ void __launch_bounds__(256) k_down(const T *__restrict__ wdt, const T *__restrict__ bdown,
+                                               const float *__restrict__ h, int hstride,
+                                               const int32_t *__restrict__ ids,
+                                               const int32_t *__restrict__ n_active, int d, int S,
+                                               int tiles, float *__restrict__ partial,
+                                               unsigned *__restrict__ tickets,
+                                               float *__restrict__ y) {
+  extern __shared__ float red[];           // [8 warps][B][256]
+  __shared__ int last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x % tiles, s = blockIdx.x / tiles;
+  const int n = *n_active;
+  const int k0 = (int)(((int64_t)s * n) / S), k1 = (int)(((int64_t)(s + 1) * n) / S);
+  const int col = tile * 256 + lane * 8;
+  const bool valid = col < d;
+  float acc[B][8];
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[b][q] = 0.f;
+  if (valid) {
+#pragma unroll 4
+    for (int k = k0 + warp; k < k1; k += 8) {
+      const int i = ids[k];
+      float wf[8];
+      WT<T>::unpack(ld_stream(wdt + (int64_t)i * d + col), wf);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const float hb = h[(int64_t)b * hstride + k];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[b][q] = fmaf(hb, wf[q], acc[b][q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) red[(warp * B + b) * 256 + lane * 8 + q] = acc[b][q];
+  __syncthreads();
+  const int c = tile * 256 + threadIdx.x;
+  if (c < d) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[(w * B + b) * 256 + threadIdx.x];
+      partial[((int64_t)s * B + b) * d + c] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&tickets[tile], 1u) == (unsigned)(S - 1));
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (c < d) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float v = 0.f;
+      for (int ss = 0; ss < S; ++ss) v += __ldcg(partial + ((int64_t)ss * B + b) * d + c);
+      if (bdown) v += WT<T>::to_float(bdown, c);
+      y[(int64_t)b * d + c] = v;
+    }
+  }
+  if (threadIdx.x == 0) tickets[tile] = 0u;   // re-arm for the next launch / graph replay
+}
+
+// ---------------------------------------------------------------------------
+// create-time repacking (not on the hot path)
+// ---------------------------------------------------------------------------
+// dst[k, dst_off + j] = src[nid[k], j] for j < cols  (rows of 16-bit elements)
+__global__ void k_gather_rows(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid,
+                              int rows, int cols, int64_t dst_stride, int dst_off,
+                              uint16_t *__restrict__ dst) {
+  const int k = blockIdx.y;
+  if (k >= rows) return;
+  const int64_t sr = nid ? nid[k] : k;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+    dst[(int64_t)k * dst_stride + dst_off + j] = src[sr * cols + j];
+}
+
+// dst[k, j] = src[j, nid[k]]: transpose-gather of nn.Linear W_down [d, m_total] into [m_local, d].
+__global__ void k_transpose_gather(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid,
+                                   int d, int m_total, int m_local, uint16_t *__restrict__ dst) {
+  __shared__ uint16_t tileb[32][33];
+  const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+    const int j = j0 + jj, k = k0 + threadIdx.x;
+    if (j < d && k < m_local) {
+      const int64_t col = nid ? nid[k] : k;
+      tileb[jj][threadIdx.x] = src[(int64_t)j * m_total + col];
+    }
+  }
+  __syncthreads();
+  for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
+    const int k = k0 + kk, j = j0 + threadIdx.x;
+    if (k < m_local && j < d) dst[(int64_t)k * d + j] = tileb[threadIdx.x][kk];
+  }
+}
+
+}  // namespace pi

@@ -1,0 +1,546 @@
+// pi_api.cu -- libpi's C ABI (include/pi.h): validation, layer handles, workspace,
+// and dispatch of the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/pi.h"
+#include "fused.cuh"
+#include "kernels.cuh"
+
+using namespace pi;
+
+// ---------------------------------------------------------------------------
+// error state
+// ---------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static pi_status fail(pi_status st, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+pi_status pi_set_error(pi_status st, const char *msg) {
+  g_err = msg;
+  return st;
+}
+
+#define PI_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(e_ == cudaErrorMemoryAllocation ? PI_ERR_OUT_OF_MEMORY : PI_ERR_CUDA, \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define PI_TRY(expr)                \
+  do {                              \
+    pi_status s_ = (expr);          \
+    if (s_ != PI_OK) return s_;     \
+  } while (0)
+
+static pi_status check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(PI_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return PI_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the handle
+// ---------------------------------------------------------------------------
+struct pi_layer {
+  int device = 0;
+  int num_sms = 148;
+  int layer_id = 0;
+  int d = 0, m_local = 0, r = 0, words = 0, max_batch = 1;
+  pi_dtype dtype = PI_DT_BF16;
+  pi_act act = PI_ACT_RELU;
+  pi_pred_act pred_act = PI_PRED_RELU;
+  uint32_t flags = 0;
+  float threshold = 0.f;
+  // library-owned weights (16-bit elements)
+  void *w_up = nullptr;    // [m_local, d] or interleaved [m_local, 2, d] (gate, up)
+  void *w_down = nullptr;  // [m_local, d] (transposed)
+  void *b_up = nullptr, *b_down = nullptr;
+  void *p_w1 = nullptr, *p_b1 = nullptr, *p_w2 = nullptr, *p_b2 = nullptr;
+  // workspace
+  float *g = nullptr;         // [max_batch, r]
+  float *scale = nullptr;     // [max_batch]
+  float *h = nullptr;         // [max_batch, m_local]
+  float *partial = nullptr;   // [S, max_batch, d]
+  unsigned *tickets = nullptr;  // [tiles]
+  uint32_t *mask = nullptr;   // [max_batch, words]
+  int32_t *ids = nullptr;     // [m_local]
+  int32_t *n_active = nullptr;
+  float *xbuf = nullptr, *ybuf = nullptr;  // [max_batch, d] each (stack ping-pong)
+  float *hx = nullptr, *hy = nullptr;      // [max_batch, d] each (host-buffer entry points)
+  FusedWork fw{};             // fused-kernel workspace
+  int tiles = 0, S = 0;
+  int64_t weight_bytes = 0, ws_bytes = 0;
+  std::vector<void *> allocs;
+};
+
+static pi_status dev_alloc(pi_layer *L, void **p, size_t bytes, bool weight) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(PI_ERR_OUT_OF_MEMORY, "layer %d: cudaMalloc(%zu) failed: %s", L->layer_id, bytes,
+                cudaGetErrorString(e));
+  }
+  L->allocs.push_back(*p);
+  (weight ? L->weight_bytes : L->ws_bytes) += (int64_t)bytes;
+  return PI_OK;
+}
+
+static void free_all(pi_layer *L) {
+  for (void *p : L->allocs) cudaFree(p);
+  L->allocs.clear();
+}
+
+// ---------------------------------------------------------------------------
+// type dispatch
+// ---------------------------------------------------------------------------
+template <int V>
+using IC = std::integral_constant<int, V>;
+template <typename T>
+struct Tag {
+  using type = T;
+};
+
+template <class F>
+static pi_status dispatch_b(int B, F &&f) {
+  switch (B) {
+    case 1: return f(IC<1>{});
+    case 2: return f(IC<2>{});
+    case 3: return f(IC<3>{});
+    case 4: return f(IC<4>{});
+    case 5: return f(IC<5>{});
+    case 6: return f(IC<6>{});
+    case 7: return f(IC<7>{});
+    case 8: return f(IC<8>{});
+  }
+  return fail(PI_ERR_INVALID_ARGUMENT, "batch %d out of range 1..%d", B, PI_MAX_BATCH);
+}
+
+template <class F>
+static pi_status dispatch_t(pi_dtype dt, F &&f) {
+  if (dt == PI_DT_F16) return f(Tag<__half>{});
+  if (dt == PI_DT_BF16) return f(Tag<__nv_bfloat16>{});
+  return fail(PI_ERR_UNSUPPORTED, "dtype %d", (int)dt);
+}
+
+// ---------------------------------------------------------------------------
+// ABI
+// ---------------------------------------------------------------------------
+extern "C" const char *pi_version(void) { return "libpi 0.1.0 sm_100a"; }
+extern "C" const char *pi_last_error(void) { return g_err.c_str(); }
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+static bool aligned2(const void *p) { return ((uintptr_t)p & 1u) == 0; }
+
+extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream, pi_layer **out) {
+  g_err.clear();
+  if (!out) return fail(PI_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (!D) return fail(PI_ERR_INVALID_ARGUMENT, "desc is NULL");
+  const int lid = D->layer_id;
+  if (D->dtype != PI_DT_F16 && D->dtype != PI_DT_BF16)
+    return fail(PI_ERR_UNSUPPORTED, "layer %d: dtype %d not supported", lid, (int)D->dtype);
+  if (D->act != PI_ACT_RELU && D->act != PI_ACT_REGLU)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: act %d", lid, (int)D->act);
+  if (D->pred_act != PI_PRED_RELU && D->pred_act != PI_PRED_LINEAR)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: pred_act %d", lid, (int)D->pred_act);
+  if (D->d <= 0 || D->m_total <= 0 || D->rank <= 0 || D->m_local <= 0)
+    return fail(PI_ERR_SHAPE, "layer %d: d=%d m_total=%d rank=%d m_local=%d must be > 0", lid, D->d,
+                D->m_total, D->rank, D->m_local);
+  if (D->d % 8 != 0) return fail(PI_ERR_ALIGNMENT, "layer %d: d=%d is not a multiple of 8", lid, D->d);
+  if (D->rank % 8 != 0)
+    return fail(PI_ERR_ALIGNMENT, "layer %d: rank=%d is not a multiple of 8", lid, D->rank);
+  if (D->m_local > D->m_total)
+    return fail(PI_ERR_SHAPE, "layer %d: m_local=%d > m_total=%d", lid, D->m_local, D->m_total);
+  if (!D->neuron_ids && D->m_local != D->m_total)
+    return fail(PI_ERR_SHAPE, "layer %d: neuron_ids NULL requires m_local == m_total (%d != %d)", lid,
+                D->m_local, D->m_total);
+  if (D->max_batch < 1 || D->max_batch > PI_MAX_BATCH)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: max_batch=%d not in 1..%d", lid, D->max_batch,
+                PI_MAX_BATCH);
+  if (D->flags & ~PI_FLAG_INPUT_RMSNORM)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: unknown flags 0x%x", lid, D->flags);
+  if (std::isnan(D->logit_threshold))
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: logit_threshold is NaN", lid);
+  if (!D->w_up || !D->w_down || !D->p_w1 || !D->p_w2)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: w_up, w_down, p_w1, p_w2 are required", lid);
+  if ((D->act == PI_ACT_REGLU) != (D->w_gate != nullptr))
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: w_gate must be given iff act == REGLU", lid);
+  const void *mats[] = {D->w_up, D->w_gate, D->w_down, D->p_w1, D->p_w2};
+  for (const void *p : mats)
+    if (p && !aligned16(p)) return fail(PI_ERR_ALIGNMENT, "layer %d: weight pointer %p not 16-B aligned", lid, p);
+  const void *vecs[] = {D->b_up, D->b_down, D->p_b1, D->p_b2};
+  for (const void *p : vecs)
+    if (p && !aligned2(p)) return fail(PI_ERR_ALIGNMENT, "layer %d: bias pointer %p not 2-B aligned", lid, p);
+  if (D->neuron_ids) {
+    for (int k = 0; k < D->m_local; ++k) {
+      const int v = D->neuron_ids[k];
+      if (v < 0 || v >= D->m_total)
+        return fail(PI_ERR_INDEX, "layer %d: neuron_ids[%d]=%d out of range [0,%d)", lid, k, v, D->m_total);
+      if (k > 0 && v <= D->neuron_ids[k - 1])
+        return fail(PI_ERR_INDEX, "layer %d: neuron_ids not strictly ascending at %d (%d after %d)", lid, k,
+                    v, D->neuron_ids[k - 1]);
+    }
+  }
+  int dev = 0;
+  PI_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  PI_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return fail(PI_ERR_UNSUPPORTED, "layer %d: device %s is sm_%d%d; libpi is built for sm_100a", lid,
+                prop.name, prop.major, prop.minor);
+
+  pi_layer *L = new pi_layer();
+  L->device = dev;
+  L->num_sms = prop.multiProcessorCount;
+  L->layer_id = lid;
+  L->d = D->d;
+  L->m_local = D->m_local;
+  L->r = D->rank;
+  L->words = (D->m_local + 31) / 32;
+  L->max_batch = D->max_batch;
+  L->dtype = D->dtype;
+  L->act = D->act;
+  L->pred_act = D->pred_act;
+  L->flags = D->flags;
+  L->threshold = D->logit_threshold;
+
+  auto cleanup = [&](pi_status st) {
+    free_all(L);
+    delete L;
+    return st;
+  };
+  const int d = L->d, ml = L->m_local, r = L->r, mt = D->m_total, MB = L->max_batch;
+  const bool reglu = L->act == PI_ACT_REGLU;
+  const size_t e = 2;
+  pi_status st = PI_OK;
+#define ALLOC(ptr, bytes, weight)                                          \
+  do {                                                                     \
+    st = dev_alloc(L, (void **)&(ptr), (size_t)(bytes), weight);           \
+    if (st != PI_OK) return cleanup(st);                                   \
+  } while (0)
+  ALLOC(L->w_up, (size_t)ml * d * e * (reglu ? 2 : 1), true);
+  ALLOC(L->w_down, (size_t)ml * d * e, true);
+  if (D->b_up) ALLOC(L->b_up, (size_t)ml * e, true);
+  if (D->b_down) ALLOC(L->b_down, (size_t)d * e, true);
+  ALLOC(L->p_w1, (size_t)r * d * e, true);
+  if (D->p_b1) ALLOC(L->p_b1, (size_t)r * e, true);
+  ALLOC(L->p_w2, (size_t)ml * r * e, true);
+  if (D->p_b2) ALLOC(L->p_b2, (size_t)ml * e, true);
+
+  // down-projection split: ~4 blocks per SM in total
+  L->tiles = (d + 255) / 256;
+  L->S = std::max(1, std::min(ml, (4 * L->num_sms + L->tiles - 1) / L->tiles));
+  ALLOC(L->g, (size_t)MB * r * 4, false);
+  ALLOC(L->scale, (size_t)MB * 4, false);
+  ALLOC(L->h, (size_t)MB * ml * 4, false);
+  ALLOC(L->partial, (size_t)L->S * MB * d * 4, false);
+  ALLOC(L->tickets, (size_t)L->tiles * 4, false);
+  ALLOC(L->mask, (size_t)MB * L->words * 4, false);
+  ALLOC(L->ids, (size_t)ml * 4, false);
+  ALLOC(L->n_active, 16, false);
+  ALLOC(L->xbuf, (size_t)MB * d * 4, false);
+  ALLOC(L->ybuf, (size_t)MB * d * 4, false);
+  ALLOC(L->hx, (size_t)MB * d * 4, false);
+  ALLOC(L->hy, (size_t)MB * d * 4, false);
+  if (!fused_alloc(L->fw, d, ml, r, MB, L->num_sms, [&](void **p, size_t bytes) {
+        return dev_alloc(L, p, bytes, false) == PI_OK;
+      }))
+    return cleanup(fail(PI_ERR_OUT_OF_MEMORY, "layer %d: fused workspace", lid));
+#undef ALLOC
+
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t *d_nid = nullptr;
+  if (D->neuron_ids) {
+    if (cudaMalloc(&d_nid, (size_t)ml * 4) != cudaSuccess)
+      return cleanup(fail(PI_ERR_OUT_OF_MEMORY, "layer %d: neuron table", lid));
+    if (cudaMemcpyAsync(d_nid, D->neuron_ids, (size_t)ml * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+      cudaFree(d_nid);
+      return cleanup(fail(PI_ERR_CUDA, "layer %d: neuron table copy", lid));
+    }
+  }
+  auto gather = [&](const void *src, void *dst, int cols, int64_t dst_stride, int dst_off) {
+    dim3 grid((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64, ml);
+    k_gather_rows<<<grid, 256, 0, s>>>((const uint16_t *)src, d_nid, ml, cols, dst_stride, dst_off,
+                                       (uint16_t *)dst);
+  };
+  if (reglu) {
+    gather(D->w_gate, L->w_up, d, 2 * (int64_t)d, 0);
+    gather(D->w_up, L->w_up, d, 2 * (int64_t)d, d);
+  } else {
+    gather(D->w_up, L->w_up, d, d, 0);
+  }
+  gather(D->p_w2, L->p_w2, r, r, 0);
+  if (D->b_up) gather(D->b_up, L->b_up, 1, 1, 0);
+  if (D->p_b2) gather(D->p_b2, L->p_b2, 1, 1, 0);
+  {
+    dim3 grid((ml + 31) / 32, (d + 31) / 32), block(32, 8);
+    k_transpose_gather<<<grid, block, 0, s>>>((const uint16_t *)D->w_down, d_nid, d, mt, ml,
+                                              (uint16_t *)L->w_down);
+  }
+  cudaMemcpyAsync(L->p_w1, D->p_w1, (size_t)r * d * e, cudaMemcpyDeviceToDevice, s);
+  if (D->p_b1) cudaMemcpyAsync(L->p_b1, D->p_b1, (size_t)r * e, cudaMemcpyDeviceToDevice, s);
+  if (D->b_down) cudaMemcpyAsync(L->b_down, D->b_down, (size_t)d * e, cudaMemcpyDeviceToDevice, s);
+  cudaMemsetAsync(L->tickets, 0, (size_t)L->tiles * 4, s);
+  cudaMemsetAsync(L->n_active, 0, 16, s);
+  fused_init(L->fw, s);
+  cudaError_t ce = cudaGetLastError();
+  if (d_nid) {
+    // the table must outlive the async gathers (create is not on the hot path)
+    cudaStreamSynchronize(s);
+    cudaFree(d_nid);
+  }
+  if (ce != cudaSuccess) return cleanup(fail(PI_ERR_CUDA, "layer %d: repack: %s", lid, cudaGetErrorString(ce)));
+  *out = L;
+  return PI_OK;
+}
+
+extern "C" pi_status pi_layer_destroy(pi_layer *L) {
+  g_err.clear();
+  if (!L) return PI_OK;
+  cudaDeviceSynchronize();
+  free_all(L);
+  delete L;
+  return PI_OK;
+}
+
+extern "C" pi_status pi_layer_get_info(const pi_layer *L, pi_layer_info *info) {
+  g_err.clear();
+  if (!L || !info) return fail(PI_ERR_INVALID_ARGUMENT, "NULL argument");
+  info->d = L->d;
+  info->m_local = L->m_local;
+  info->rank = L->r;
+  info->max_batch = L->max_batch;
+  info->mask_words = L->words;
+  info->dtype = L->dtype;
+  info->act = L->act;
+  info->pred_act = L->pred_act;
+  info->flags = L->flags;
+  info->num_sms = L->num_sms;
+  info->weight_bytes = L->weight_bytes;
+  info->workspace_bytes = L->ws_bytes;
+  info->launches_per_forward =
+      fused_supported(L->fw) ? 1 : 5 + ((L->flags & PI_FLAG_INPUT_RMSNORM) ? 1 : 0);
+  return PI_OK;
+}
+
+static pi_status check_common(const pi_layer *L, int B) {
+  if (!L) return fail(PI_ERR_INVALID_ARGUMENT, "layer handle is NULL");
+  if (B < 1 || B > L->max_batch)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: batch %d not in 1..max_batch=%d", L->layer_id, B,
+                L->max_batch);
+  return PI_OK;
+}
+
+// scale pointer for the RMS flag (launches the scale kernel) or NULL
+static const float *launch_scale(pi_layer *L, const float *x, int B, cudaStream_t s) {
+  if (!(L->flags & PI_FLAG_INPUT_RMSNORM)) return nullptr;
+  k_rms_scale<<<B, 256, 0, s>>>(x, L->d, L->scale);
+  return L->scale;
+}
+
+static pi_status run_predict(pi_layer *L, const float *x, int B, const float *scale, uint32_t *mask,
+                             float *logits, cudaStream_t s) {
+  return dispatch_t(L->dtype, [&](auto tt) {
+    using T = typename decltype(tt)::type;
+    return dispatch_b(B, [&](auto bb) {
+      constexpr int NB = decltype(bb)::value;
+      const int g1 = (L->r + 1) / 2;
+      if (L->pred_act == PI_PRED_RELU)
+        k_predict1<T, NB, true><<<g1, 256, 0, s>>>((const T *)L->p_w1, (const T *)L->p_b1, x, scale, L->r,
+                                                   L->d, L->g);
+      else
+        k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)L->p_w1, (const T *)L->p_b1, x, scale, L->r,
+                                                    L->d, L->g);
+      PI_TRY(check_launch("predict1"));
+      const size_t smem = (size_t)(NB * L->r + 4 * NB * 32) * 4;
+      if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_predict2<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      }
+      k_predict2<T, NB><<<(L->words + 3) / 4, 128, smem, s>>>((const T *)L->p_w2, (const T *)L->p_b2, L->g,
+                                                               L->threshold, L->m_local, L->r, L->words,
+                                                               mask, logits);
+      return check_launch("predict2");
+    });
+  });
+}
+
+static pi_status run_ffn(pi_layer *L, const float *x, int B, const float *scale, const int32_t *ids,
+                         const int32_t *n_active, const uint32_t *mask, float *y, cudaStream_t s) {
+  return dispatch_t(L->dtype, [&](auto tt) {
+    using T = typename decltype(tt)::type;
+    return dispatch_b(B, [&](auto bb) {
+      constexpr int NB = decltype(bb)::value;
+      const int gup = std::max(1, std::min((L->m_local + 7) / 8, L->num_sms * 8));
+      if (L->act == PI_ACT_REGLU)
+        k_up<T, NB, true><<<gup, 256, 0, s>>>((const T *)L->w_up, (const T *)L->b_up, x, scale, ids, n_active,
+                                              mask, L->words, L->d, L->h, L->m_local);
+      else
+        k_up<T, NB, false><<<gup, 256, 0, s>>>((const T *)L->w_up, (const T *)L->b_up, x, scale, ids,
+                                               n_active, mask, L->words, L->d, L->h, L->m_local);
+      PI_TRY(check_launch("up"));
+      const size_t smem = (size_t)8 * NB * 256 * 4;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_down<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_down<T, NB><<<L->tiles * L->S, 256, smem, s>>>((const T *)L->w_down, (const T *)L->b_down, L->h,
+                                                       L->m_local, ids, n_active, L->d, L->S, L->tiles,
+                                                       L->partial, L->tickets, y);
+      return check_launch("down");
+    });
+  });
+}
+
+extern "C" pi_status pi_predict(pi_layer *L, const float *x, int32_t B, uint32_t *mask, float *logits,
+                                pi_stream_t stream) {
+  g_err.clear();
+  PI_TRY(check_common(L, B));
+  if (!x || !mask) return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: x and mask are required", L->layer_id);
+  if (!aligned16(x)) return fail(PI_ERR_ALIGNMENT, "layer %d: x not 16-B aligned", L->layer_id);
+  cudaStream_t s = (cudaStream_t)stream;
+  const float *scale = launch_scale(L, x, B, s);
+  return run_predict(L, x, B, scale, mask, logits, s);
+}
+
+extern "C" pi_status pi_compact(pi_layer *L, const uint32_t *mask, int32_t B, int32_t *ids,
+                                int32_t *n_active, pi_stream_t stream) {
+  g_err.clear();
+  PI_TRY(check_common(L, B));
+  if (!mask || !ids || !n_active)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: mask, ids, n_active are required", L->layer_id);
+  k_compact<<<1, 1024, 0, (cudaStream_t)stream>>>(mask, B, L->words, ids, n_active);
+  return check_launch("compact");
+}
+
+extern "C" pi_status pi_sparse_ffn(pi_layer *L, const float *x, int32_t B, const int32_t *ids,
+                                   const int32_t *n_active, const uint32_t *mask, float *y,
+                                   pi_stream_t stream) {
+  g_err.clear();
+  PI_TRY(check_common(L, B));
+  if (!x || !ids || !n_active || !y)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: x, ids, n_active, y are required", L->layer_id);
+  if (!mask && B != 1)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: mask may be NULL only for B == 1 (B=%d)", L->layer_id, B);
+  if (!aligned16(x) || !aligned16(y))
+    return fail(PI_ERR_ALIGNMENT, "layer %d: x and y must be 16-B aligned", L->layer_id);
+  cudaStream_t s = (cudaStream_t)stream;
+  const float *scale = launch_scale(L, x, B, s);
+  return run_ffn(L, x, B, scale, ids, n_active, mask, y, s);
+}
+
+static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint32_t *mask_out,
+                             int32_t *ids_out, int32_t *n_out, cudaStream_t s) {
+  if (fused_supported(L->fw)) {
+    return dispatch_t(L->dtype, [&](auto tt) {
+      using T = typename decltype(tt)::type;
+      FusedArgs a{};
+      a.w_up = L->w_up; a.w_down = L->w_down; a.b_up = L->b_up; a.b_down = L->b_down;
+      a.p_w1 = L->p_w1; a.p_b1 = L->p_b1; a.p_w2 = L->p_w2; a.p_b2 = L->p_b2;
+      a.x = x; a.y = y; a.d = L->d; a.m = L->m_local; a.r = L->r; a.words = L->words; a.B = B;
+      a.threshold = L->threshold; a.rmsnorm = (L->flags & PI_FLAG_INPUT_RMSNORM) != 0;
+      a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
+      a.mask_out = mask_out; a.ids_out = ids_out; a.n_out = n_out;
+      cudaError_t e = fused_launch<T>(L->fw, a, L->num_sms, s);
+      if (e != cudaSuccess) return fail(PI_ERR_CUDA, "layer %d: fused launch: %s", L->layer_id, cudaGetErrorString(e));
+      return PI_OK;
+    });
+  }
+  uint32_t *mask = mask_out ? mask_out : L->mask;
+  int32_t *ids = ids_out ? ids_out : L->ids;
+  int32_t *n = n_out ? n_out : L->n_active;
+  const float *scale = launch_scale(L, x, B, s);
+  PI_TRY(run_predict(L, x, B, scale, mask, nullptr, s));
+  k_compact<<<1, 1024, 0, s>>>(mask, B, L->words, ids, n);
+  PI_TRY(check_launch("compact"));
+  return run_ffn(L, x, B, scale, ids, n, mask, y, s);
+}
+
+extern "C" pi_status pi_layer_forward(pi_layer *L, const float *x, int32_t B, float *y, uint32_t *mask_out,
+                                      int32_t *ids_out, int32_t *n_active_out, pi_stream_t stream) {
+  g_err.clear();
+  PI_TRY(check_common(L, B));
+  if (!x || !y) return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: x and y are required", L->layer_id);
+  if (!aligned16(x) || !aligned16(y))
+    return fail(PI_ERR_ALIGNMENT, "layer %d: x and y must be 16-B aligned", L->layer_id);
+  return forward_dev(L, x, B, y, mask_out, ids_out, n_active_out, (cudaStream_t)stream);
+}
+
+extern "C" pi_status pi_layer_forward_host(pi_layer *L, const float *x_host, int32_t B, float *y_host,
+                                           pi_stream_t stream) {
+  g_err.clear();
+  PI_TRY(check_common(L, B));
+  if (!x_host || !y_host) return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: x_host and y_host are required", L->layer_id);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)B * L->d * 4;
+  PI_CUDA(cudaMemcpyAsync(L->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+  PI_TRY(forward_dev(L, L->hx, B, L->hy, nullptr, nullptr, nullptr, s));
+  PI_CUDA(cudaMemcpyAsync(y_host, L->hy, bytes, cudaMemcpyDeviceToHost, s));
+  PI_CUDA(cudaStreamSynchronize(s));
+  return PI_OK;
+}
+
+static pi_status stack_check(pi_layer *const *layers, int32_t n_layers, int32_t B) {
+  if (!layers || n_layers < 1) return fail(PI_ERR_INVALID_ARGUMENT, "stack: NULL layers or n_layers < 1");
+  for (int l = 0; l < n_layers; ++l) {
+    PI_TRY(check_common(layers[l], B));
+    if (layers[l]->d != layers[0]->d)
+      return fail(PI_ERR_SHAPE, "stack: layer %d has d=%d, layer 0 has d=%d", layers[l]->layer_id,
+                  layers[l]->d, layers[0]->d);
+  }
+  return PI_OK;
+}
+
+static pi_status stack_dev(pi_layer *const *layers, int32_t n_layers, const float *x, int32_t B, float *y,
+                           int32_t *n_out, cudaStream_t s) {
+  float *buf[2] = {layers[0]->xbuf, layers[0]->ybuf};
+  const float *cur = x;
+  for (int l = 0; l < n_layers; ++l) {
+    float *dst = (l == n_layers - 1) ? y : buf[l & 1];
+    if (cur == dst) dst = buf[(l + 1) & 1];
+    PI_TRY(forward_dev(layers[l], cur, B, dst, nullptr, nullptr, n_out ? n_out + l : nullptr, s));
+    cur = dst;
+  }
+  if (cur != y) PI_CUDA(cudaMemcpyAsync(y, cur, (size_t)B * layers[0]->d * 4, cudaMemcpyDeviceToDevice, s));
+  return PI_OK;
+}
+
+extern "C" pi_status pi_stack_forward(pi_layer *const *layers, int32_t n_layers, const float *x, int32_t B,
+                                      float *y, int32_t *n_active_out, pi_stream_t stream) {
+  g_err.clear();
+  if (!x || !y) return fail(PI_ERR_INVALID_ARGUMENT, "stack: NULL x or y");
+  PI_TRY(stack_check(layers, n_layers, B));
+  if (!aligned16(x) || !aligned16(y)) return fail(PI_ERR_ALIGNMENT, "stack: x and y must be 16-B aligned");
+  return stack_dev(layers, n_layers, x, B, y, n_active_out, (cudaStream_t)stream);
+}
+
+extern "C" pi_status pi_stack_forward_host(pi_layer *const *layers, int32_t n_layers, const float *x_host,
+                                           int32_t B, float *y_host, pi_stream_t stream) {
+  g_err.clear();
+  if (!x_host || !y_host) return fail(PI_ERR_INVALID_ARGUMENT, "stack: NULL x_host or y_host");
+  PI_TRY(stack_check(layers, n_layers, B));
+  cudaStream_t s = (cudaStream_t)stream;
+  pi_layer *L0 = layers[0];
+  const size_t bytes = (size_t)B * L0->d * 4;
+  PI_CUDA(cudaMemcpyAsync(L0->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+  PI_TRY(stack_dev(layers, n_layers, L0->hx, B, L0->hy, nullptr, s));
+  PI_CUDA(cudaMemcpyAsync(y_host, L0->hy, bytes, cudaMemcpyDeviceToHost, s));
+  PI_CUDA(cudaStreamSynchronize(s));
+  return PI_OK;
+}

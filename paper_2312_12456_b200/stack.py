@@ -1,0 +1,127 @@
+"""Multi-layer, optionally neuron-sharded decode stacks over libpi handles.
+
+The paper keeps hot neurons on the GPU and cold ones on the CPU, computing
+each unit's predicted-active neurons independently and merging the partial
+outputs with an add on the GPU.  Here the units are G
+identical B200s: ``pi_partition`` places each layer's neurons (equal counts,
+balanced expected activity), every rank owns one shard of every layer, and the
+merge is one NCCL all-reduce(sum) of the fp32 [B, d] partials per layer over
+NVLink.  b_down lives on rank 0 only, so it is added once.
+
+Everything numeric runs in libpi's kernels; this module only builds handles and
+sequences calls (plus the NCCL collective).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import gen
+from . import pi
+
+
+@dataclasses.dataclass
+class LayerMeta:
+    """What the bench needs to count algorithmic bytes for one layer shard."""
+    d: int
+    m_local: int
+    r: int
+    reglu: bool
+    b_up: bool
+    b_down: bool          # this shard owns b_down
+    p_b1: bool
+    p_b2: bool
+    e: int = 2            # bytes per weight element
+
+
+class Stack:
+    def __init__(self, layers: List[pi.Layer], metas: List[LayerMeta], rank: int = 0, world: int = 1,
+                 group=None):
+        self.layers = layers
+        self.metas = metas
+        self.rank = rank
+        self.world = world
+        self.group = group
+        self.handles = pi.handles(layers)
+        self.d = layers[0].d
+
+    def __len__(self):
+        return len(self.layers)
+
+    def step(self, x: torch.Tensor, y: torch.Tensor, n_out: Optional[torch.Tensor] = None,
+             bufs: Optional[List[torch.Tensor]] = None):
+        """One decode step for B tokens through every layer.  World size 1: one pi_stack_forward
+        call.  World size > 1: per layer pi_layer_forward on the local shard, then all-reduce."""
+        if self.world == 1:
+            pi.pi_stack_forward(self.handles, x, y, n_out)
+            return y
+        cur = x
+        for l, L in enumerate(self.layers):
+            dst = y if l == len(self.layers) - 1 else bufs[l & 1]
+            L.forward(cur, dst, None, None, None if n_out is None else n_out[l:l + 1])
+            dist.all_reduce(dst, op=dist.ReduceOp.SUM, group=self.group)
+            cur = dst
+        return y
+
+    def close(self):
+        for L in self.layers:
+            L.close()
+
+
+def shard_ids(p: np.ndarray, world: int, rank: int, granule: int = 64) -> Optional[np.ndarray]:
+    if world == 1:
+        return None
+    m = len(p)
+    g = granule if m % (granule * world) == 0 else 1
+    owner, sids, off = pi.pi_partition(p.astype(np.float32), world, g)
+    return sids[off[rank]:off[rank + 1]].copy()
+
+
+def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, world: int = 1, seed: int = 0,
+                device="cuda", max_batch: int = 1, mean_act: float = 0.10, group=None,
+                keep_weights: bool = False, dims: Optional[dict] = None):
+    """Generate the config's layers (random init, seeded) and create this rank's handles.
+
+    Returns (Stack, weights-or-None).  With keep_weights the generator tensors stay alive
+    (tests and the oracle baseline read them); otherwise each layer's global tensors are freed
+    once the library has its own repacked copy."""
+    L = n_layers or cfg.layers
+    flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
+    layers, metas, kept = [], [], []
+    dims = dims or {}
+    for l in range(L):
+        w = gen.make_layer(cfg, layer=l, seed=seed, device=device, mean_act=mean_act, **dims)
+        nid = shard_ids(w.p, world, rank)
+        own = rank == 0
+        layers.append(pi.Layer(w, neuron_ids=nid, max_batch=max_batch, flags=flags, layer_id=l, own_b_down=own))
+        m_local = w.m if nid is None else len(nid)
+        metas.append(LayerMeta(w.d, m_local, w.r, w.act == "reglu", w.b_up is not None,
+                               own and w.b_down is not None, w.p_b1 is not None, w.p_b2 is not None))
+        if keep_weights:
+            kept.append((w, nid))
+        else:
+            del w
+    if not keep_weights:
+        torch.cuda.empty_cache()
+    return Stack(layers, metas, rank, world, group), (kept if keep_weights else None)
+
+
+def algorithmic_bytes(meta: LayerMeta, n_union: int, B: int) -> int:
+    """Algorithmic HBM bytes of one layer-step on one shard; counted from the
+    realised union count.  Split-K partials, re-reads and over-fetch are NOT algorithmic."""
+    e, d, r, m = meta.e, meta.d, meta.r, meta.m_local
+    c = 3 if meta.reglu else 2
+    w = e * (r * d + r * m + (r if meta.p_b1 else 0) + (m if meta.p_b2 else 0))
+    w += e * c * n_union * d + (e * n_union if meta.b_up else 0) + (e * d if meta.b_down else 0)
+    words = (m + 31) // 32
+    io = 4 * B * d + 4 * B * d + 4 * B * words + 2 * 4 * n_union + 4 * B * r
+    return int(w + io)
+
+
+def algorithmic_flops(meta: LayerMeta, n_union: int, B: int) -> int:
+    c = 3 if meta.reglu else 2
+    return int(2 * B * (meta.r * meta.d + meta.r * meta.m_local + (c - 1) * n_union * meta.d + n_union * meta.d))

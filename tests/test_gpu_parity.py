@@ -1,0 +1,410 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Tolerances (BASELINE.json north_star): masks and ids bit-exact except neurons whose oracle
+logit lies within 1e-4 of the threshold; outputs rel-L2 <= 1e-3 (plus an internal regression
+gate at 1e-5), computed with the oracle fed the GPU's own ids and
+mask bits.  Integer-exact layers must match bit for bit.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ffn as O
+from oracle import partition as OP
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+GATE = 1e-5
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2312_12456_b200 import gen, pi
+    torch.cuda.set_device(0)
+    return gen, pi
+
+
+def f(t):
+    return None if t is None else t.float().cpu().numpy()
+
+
+def run_forward(pi, L, x, fused=True):
+    """Whole hot path through pi_layer_forward; returns (y, mask bool, ids, n)."""
+    B = x.shape[0]
+    y = torch.full((B, L.d), float("nan"), device=x.device)
+    mask = L.new_mask(B)
+    ids = L.new_ids()
+    n = torch.full((1,), -1, dtype=torch.int32, device=x.device)
+    L.forward(x, y, mask, ids, n)
+    torch.cuda.synchronize()
+    nn = int(n.item())
+    return y.cpu().numpy(), O.unpack_mask(mask.cpu().numpy().view(np.uint32), L.m_local), \
+        ids[:nn].cpu().numpy(), nn
+
+
+def run_steps(pi, L, x):
+    """The same path as three ABI calls: pi_predict -> pi_compact -> pi_sparse_ffn."""
+    B = x.shape[0]
+    mask = L.new_mask(B)
+    logits = torch.empty(B, L.m_local, device=x.device)
+    ids = L.new_ids()
+    n = torch.zeros(1, dtype=torch.int32, device=x.device)
+    y = torch.full((B, L.d), float("nan"), device=x.device)
+    L.predict(x, mask, logits)
+    L.compact(mask, B, ids, n)
+    L.sparse_ffn(x, ids, n, mask, y)
+    torch.cuda.synchronize()
+    nn = int(n.item())
+    return (y.cpu().numpy(), O.unpack_mask(mask.cpu().numpy().view(np.uint32), L.m_local),
+            ids[:nn].cpu().numpy(), nn, logits.cpu().numpy())
+
+
+def oracle_check(w, x, y, gmask, gids, norm=False, nid=None, with_bdown=True, tol=TOL, gate=GATE):
+    """Checks GPU outputs against the oracle; returns (rel_l2, n_band_flips)."""
+    xo = f(x).astype(np.float64)
+    if norm:
+        xo = O.rms_normalize(xo)
+    sel = slice(None) if nid is None else np.asarray(nid)
+    p_w2, p_b2 = f(w.p_w2)[sel], (None if w.p_b2 is None else f(w.p_b2)[sel])
+    om, z = O.predict(xo, f(w.p_w1), f(w.p_b1), p_w2, p_b2, w.threshold, w.pred_act)
+    band = O.near_threshold(z, w.threshold)
+    assert ((gmask == om) | band).all(), f"mask mismatch outside band: {np.argwhere((gmask != om) & ~band)[:5]}"
+    assert (gids == O.compact(gmask)).all()
+    w_up = f(w.w_up)[sel]
+    w_gate = None if w.w_gate is None else f(w.w_gate)[sel]
+    w_down = f(w.w_down)[:, sel]
+    b_up = None if w.b_up is None else f(w.b_up)[sel]
+    yo = O.sparse_ffn(xo, gids, gmask, w_up, b_up, w_gate, w_down, f(w.b_down) if with_bdown else None, w.act)
+    err = O.rel_l2(y, yo)
+    assert err <= tol, f"rel-L2 {err:.3e} > {tol}"
+    assert err <= gate, f"rel-L2 {err:.3e} above the internal regression gate {gate}"
+    return err, int(((gmask != om) & band).sum())
+
+
+# ---------------------------------------------------------------------------
+# golden worked example (fig:example P:477-505), embedded in d = 8, r = 8 with zero padding
+# ---------------------------------------------------------------------------
+def _golden_layer(gen, act="relu", b_down=None, dtype=torch.bfloat16):
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "fig_example.json")))
+    d, m, r = 8, 8, 8
+
+    def pad(a, rows, cols):
+        out = torch.zeros(rows, cols)
+        a = torch.tensor(a, dtype=torch.float32)
+        out[: a.shape[0], : a.shape[1]] = a
+        return out
+
+    gate = pad(g["w_up"], m, d)
+    up = pad(g["cases"]["G6_reglu"]["w_up_reglu"], m, d) if act == "reglu" else gate
+    wdT = pad(g["w_down_T"], m, d)
+    cuda = lambda t: t.to(dtype).cuda().contiguous()  # noqa: E731
+    w = gen.LayerWeights(d, m, r, act, cuda(up), cuda(gate) if act == "reglu" else None, cuda(wdT.T.contiguous()),
+                         None, None if b_down is None else cuda(torch.tensor(b_down + [0] * (d - len(b_down)),
+                                                                                dtype=torch.float32)),
+                         cuda(pad(g["p_w1"], r, d)), None, cuda(pad(g["p_w2"], m, r)), None,
+                         g["threshold"], "relu", None)
+    return g, w
+
+
+def _x8(rows):
+    x = torch.zeros(len(rows), 8)
+    x[:, :2] = torch.tensor(rows, dtype=torch.float32)
+    return x.cuda()
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_golden_g1_g2_g3(env, dtype):
+    gen, pi = env
+    g, w = _golden_layer(gen, dtype=dtype)
+    L = pi.Layer(w, max_batch=2)
+    y, gm, ids, n, logits = run_steps(pi, L, _x8([[1, 2]]))
+    c = g["cases"]
+    assert (logits[0] == np.array(c["G1_predict"]["z"][0])).all()
+    assert O.pack_mask(gm).tolist() == c["G1_predict"]["mask_words"]
+    assert ids.tolist() == c["G1_predict"]["ids"]
+    assert (y[0, :2] == np.array(c["G2_sparse_ffn"]["y"][0])).all() and (y[0, 2:] == 0).all()
+    y2, gm2, ids2, n2 = run_forward(pi, L, _x8([[1, 2]]))
+    assert (y2 == y).all() and ids2.tolist() == [3, 4, 5]
+    # G3: all-ones prediction (t = -inf) gives the dense answer
+    Lall = pi.Layer(w, max_batch=1, threshold=float("-inf"))
+    y3, _, ids3, _ = run_forward(pi, Lall, _x8([[1, 2]]))
+    assert ids3.tolist() == list(range(8))
+    assert (y3[0, :2] == np.array(c["G3_invariants"]["y_dense"][0])).all()
+
+
+def test_golden_g4_shards_g5_bias(env):
+    gen, pi = env
+    g, w = _golden_layer(gen, b_down=[100, 0])
+    c = g["cases"]["G4_shards"]
+    parts = []
+    for k, key in enumerate(("shard_fast", "shard_slow")):
+        s = c[key]
+        L = pi.Layer(w, neuron_ids=s["neuron_ids"], own_b_down=(k == 0))
+        y, gm, ids, n = run_forward(pi, L, _x8([[1, 2]]))
+        assert O.pack_mask(gm).tolist() == s["mask_words"]
+        assert ids.tolist() == s["local_ids"]
+        exp = np.array(s["y"][0], dtype=np.float64) + (np.array([100, 0]) if k == 0 else 0)
+        assert (y[0, :2] == exp).all()
+        parts.append(y)
+    assert (O.merge(parts)[0, :2] == np.array(g["cases"]["G5_b_down"]["y"][0])).all()
+
+
+def test_golden_g6_reglu_g7_batch(env):
+    gen, pi = env
+    g, w = _golden_layer(gen, act="reglu")
+    L = pi.Layer(w, max_batch=2)
+    y, gm, ids, n = run_forward(pi, L, _x8([[1, 2]]))
+    assert (y[0, :2] == np.array(g["cases"]["G6_reglu"]["y"][0])).all()
+    g, w = _golden_layer(gen)
+    L = pi.Layer(w, max_batch=2)
+    c = g["cases"]["G7_batch2"]
+    y, gm, ids, n = run_forward(pi, L, _x8(c["x"]))
+    assert O.pack_mask(gm).tolist() == c["mask_words"]
+    assert ids.tolist() == c["union_ids"]
+    assert (y[:, :2] == np.array(c["y"])).all()
+
+
+# ---------------------------------------------------------------------------
+# integer-exact layers: bitwise equality, several tiles and ragged tails
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("act,shape", [("relu", (256, 1000, 64)), ("relu", (136, 777, 24)),
+                                       ("reglu", (64, 250, 16)), ("reglu", (40, 97, 8))])
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("B", [1, 3, 8])
+def test_integer_layers_bitwise(env, act, shape, dtype, B):
+    gen, pi = env
+    d, m, r = shape
+    w = gen.make_int_layer(d, m, r, act, seed=d + m + B, dtype=dtype, device="cuda")
+    x = gen.int_tokens(B, d, act, seed=B).cuda()
+    L = pi.Layer(w, max_batch=8)
+    for runner in ("steps", "fused"):
+        if runner == "steps":
+            y, gm, ids, n, logits = run_steps(pi, L, x)
+        else:
+            y, gm, ids, n = run_forward(pi, L, x)
+        xo = f(x).astype(np.float64)
+        om, z = O.predict(xo, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), 0.5)
+        assert (gm == om).all()
+        if runner == "steps":
+            assert (logits == z).all()
+        assert (ids == O.compact(om)).all() and n == len(O.compact(om))
+        yo = O.sparse_ffn(xo, ids, om, f(w.w_up), f(w.b_up), f(w.w_gate), f(w.w_down), f(w.b_down), act)
+        assert (y == yo).all(), runner
+
+
+# ---------------------------------------------------------------------------
+# random layers with the configs' shape classes (reduced m for speed), several batches
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,dims", [("c1", (768, 3072, 64)), ("c2", (4096, 2048, 256)),
+                                       ("c3", (5120, 1400, 320)), ("c4", (8192, 1024, 512)),
+                                       ("c5", (12288, 520, 768))])
+@pytest.mark.parametrize("B", [1, 4])
+def test_random_layers(env, name, dims, B):
+    gen, pi = env
+    cfg = gen.CONFIGS[name]
+    d, m, r = dims
+    w = gen.make_layer(cfg, seed=7, device="cuda", d=d, m=m, r=r)
+    flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
+    L = pi.Layer(w, max_batch=8, flags=flags)
+    x = gen.tokens(B, d, seed=11, device="cuda") * (3.0 if cfg.rmsnorm else 1.0)
+    y, gm, ids, n = run_forward(pi, L, x)
+    oracle_check(w, x, y, gm, ids, norm=cfg.rmsnorm)
+    y2, gm2, ids2, n2, _ = run_steps(pi, L, x)
+    assert (gm2 == gm).all() and (ids2 == ids).all()
+    oracle_check(w, x, y2, gm2, ids2, norm=cfg.rmsnorm)
+
+
+@pytest.mark.parametrize("B", [1, 2, 8])
+def test_mode_t_masks_compact_and_ffn(env, B):
+    """Bernoulli masks (mode T) fed straight to pi_compact and pi_sparse_ffn."""
+    gen, pi = env
+    cfg = gen.CONFIGS["c4"]
+    d, m, r = 2048, 4000, 64
+    w = gen.make_layer(cfg, seed=3, device="cuda", d=d, m=m, r=r)
+    L = pi.Layer(w, max_batch=8)
+    mk = gen.bernoulli_masks(gen.activity_profile(m, 0.1, seed=3), B, seed=4)
+    words = gen.pack_bits(mk).cuda()
+    ids = L.new_ids()
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L.compact(words, B, ids, n)
+    x = gen.tokens(B, d, seed=5, device="cuda")
+    y = torch.empty(B, d, device="cuda")
+    L.sparse_ffn(x, ids, n, words, y)
+    torch.cuda.synchronize()
+    nn = int(n.item())
+    gids = ids[:nn].cpu().numpy()
+    assert (gids == O.compact(mk.numpy())).all()
+    yo = O.sparse_ffn(f(x), gids, mk.numpy(), f(w.w_up), None, None, f(w.w_down), None, "relu")
+    assert O.rel_l2(y.cpu().numpy(), yo) <= GATE
+
+
+# ---------------------------------------------------------------------------
+# edge cases
+# ---------------------------------------------------------------------------
+def test_empty_mask_gives_bias_or_zero(env):
+    gen, pi = env
+    for name in ("c1", "c4"):
+        cfg = gen.CONFIGS[name]
+        w = gen.make_layer(cfg, seed=1, device="cuda", d=512, m=700, r=32)
+        L = pi.Layer(w, max_batch=4, threshold=float("inf"))
+        x = gen.tokens(3, 512, device="cuda")
+        y, gm, ids, n = run_forward(pi, L, x)
+        assert n == 0 and not gm.any()
+        exp = np.zeros((3, 512)) if w.b_down is None else np.tile(f(w.b_down), (3, 1))
+        assert (y == exp).all()
+        y2, *_ = run_steps(pi, L, x)
+        assert (y2 == exp).all()
+
+
+def test_full_mask_equals_dense(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c2"]
+    w = gen.make_layer(cfg, seed=2, device="cuda", d=1024, m=2500, r=64)
+    L = pi.Layer(w, max_batch=2, threshold=float("-inf"))
+    x = gen.tokens(2, 1024, device="cuda")
+    y, gm, ids, n = run_forward(pi, L, x)
+    assert n == 2500 and gm.all()
+    yd = O.dense_ffn(f(x), f(w.w_up), f(w.b_up), None, f(w.w_down), f(w.b_down))
+    assert O.rel_l2(y, yd) <= GATE
+
+
+def test_nan_logits_inactive(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c1"]
+    w = gen.make_layer(cfg, seed=2, device="cuda", d=256, m=300, r=32)
+    w.p_b2[5] = float("nan")
+    w.p_b2[77] = float("inf")
+    L = pi.Layer(w, max_batch=1, threshold=float("-inf"))
+    y, gm, ids, n = run_forward(pi, L, gen.tokens(1, 256, device="cuda"))
+    assert not gm[0, 5] and gm[0, 77] and n == 299
+
+
+def test_determinism_bitwise(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c3"]
+    w = gen.make_layer(cfg, seed=9, device="cuda", d=2048, m=4096, r=128)
+    L = pi.Layer(w, max_batch=8, flags=pi.PI_FLAG_INPUT_RMSNORM)
+    x = gen.tokens(8, 2048, device="cuda")
+    ref = run_forward(pi, L, x)[0]
+    for _ in range(20):
+        assert (run_forward(pi, L, x)[0] == ref).all()
+
+
+def test_batch_invariance(env):
+    """Batched result == each token alone (per-token masks; reading R9)."""
+    gen, pi = env
+    cfg = gen.CONFIGS["c3"]
+    w = gen.make_layer(cfg, seed=4, device="cuda", d=1024, m=2000, r=64)
+    L = pi.Layer(w, max_batch=8, flags=pi.PI_FLAG_INPUT_RMSNORM)
+    x = gen.tokens(8, 1024, device="cuda")
+    y, gm, ids, n = run_forward(pi, L, x)
+    for b in (0, 5, 7):
+        yb, gmb, idsb, nb = run_forward(pi, L, x[b:b + 1].contiguous())
+        assert (gmb[0] == gm[b]).all()
+        assert O.rel_l2(yb[0], y[b]) <= GATE
+
+
+def test_host_path_equals_device_path(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c2"]
+    w = gen.make_layer(cfg, seed=5, device="cuda", d=1024, m=4096, r=64)
+    L = pi.Layer(w, max_batch=4)
+    x = gen.tokens(4, 1024, device="cuda")
+    yd = run_forward(pi, L, x)[0]
+    xh = x.cpu().pin_memory()
+    yh = torch.empty(4, 1024).pin_memory()
+    L.forward_host(xh, yh)
+    assert (yh.numpy() == yd).all()
+
+
+def test_stack_equals_chained_layers(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c4"]
+    d, m, r = 1024, 3000, 64
+    ws = [gen.make_layer(cfg, layer=l, seed=1, device="cuda", d=d, m=m, r=r) for l in range(3)]
+    Ls = [pi.Layer(w, max_batch=2, flags=pi.PI_FLAG_INPUT_RMSNORM, layer_id=l) for l, w in enumerate(ws)]
+    x = gen.tokens(2, d, device="cuda")
+    y = torch.empty(2, d, device="cuda")
+    pi.pi_stack_forward(Ls, x, y)
+    cur = x
+    for l, L in enumerate(Ls):
+        yl, gm, ids, n = run_forward(pi, L, cur)
+        oracle_check(ws[l], cur, yl, gm, ids, norm=True)   # per layer on the GPU's own input (R20)
+        cur = torch.from_numpy(yl).cuda()
+    assert (y.cpu().numpy() == cur.cpu().numpy()).all()
+
+
+def test_sharded_emulation_merge(env):
+    """G shards on one GPU (pi_partition placement, b_down on shard 0): the merged partials equal
+    the unsharded result (O5)."""
+    gen, pi = env
+    cfg = gen.CONFIGS["c5"]
+    d, m, r = 1024, 4096, 64
+    w = gen.make_layer(cfg, seed=8, device="cuda", d=d, m=m, r=r)
+    x = gen.tokens(1, d, device="cuda")
+    L = pi.Layer(w)
+    y_full, gm_full, ids_full, _ = run_forward(pi, L, x)
+    for G in (2, 4, 8):
+        owner, sids, off = pi.pi_partition(w.p.astype(np.float32), G, 64)
+        parts = []
+        for g in range(G):
+            nid = sids[off[g]:off[g + 1]]
+            Lg = pi.Layer(w, neuron_ids=nid, own_b_down=(g == 0))
+            yg, gmg, idsg, ng = run_forward(pi, Lg, x)
+            oracle_check(w, x, yg, gmg, idsg, nid=nid, with_bdown=(g == 0))
+            assert (gmg[0] == gm_full[0][nid]).all()
+            parts.append(yg)
+        assert O.rel_l2(O.merge(parts), y_full) <= GATE
+
+
+def test_partition_then_shard_cover(env):
+    gen, pi = env
+    p = gen.activity_profile(32768, 0.1, seed=0).astype(np.float32)
+    owner, sids, off = pi.pi_partition(p, 8, 64)
+    OP.check_partition(owner.tolist(), sids.tolist(), off.tolist(), 32768, 8, 64)
+
+
+def test_error_paths(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c1"]
+    w = gen.make_layer(cfg, seed=1, device="cuda", d=256, m=512, r=32)
+    L = pi.Layer(w, max_batch=2)
+    x = gen.tokens(3, 256, device="cuda")
+    with pytest.raises(pi.PiError) as e:
+        L.forward(x, torch.empty(3, 256, device="cuda"))
+    assert e.value.name == "PI_ERR_INVALID_ARGUMENT"
+    xb = torch.zeros(2 * 256 + 1, device="cuda")[1:].view(2, 256)
+    with pytest.raises(pi.PiError) as e:
+        L.forward(xb, torch.empty(2, 256, device="cuda"))
+    assert e.value.name == "PI_ERR_ALIGNMENT"
+    with pytest.raises(pi.PiError) as e:
+        L.sparse_ffn(x[:2].contiguous(), L.new_ids(), torch.zeros(1, dtype=torch.int32, device="cuda"), None,
+                     torch.empty(2, 256, device="cuda"))
+    assert e.value.name == "PI_ERR_INVALID_ARGUMENT"
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE sizes, the bench's launch configuration (one layer each; every output checked)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_full_size_layers(env, name):
+    gen, pi = env
+    cfg = gen.CONFIGS[name]
+    w = gen.make_layer(cfg, seed=0, device="cuda")
+    flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
+    B = 8 if name == "c3" else 1
+    L = pi.Layer(w, max_batch=B, flags=flags)
+    x = gen.tokens(B, cfg.d, seed=1, device="cuda")
+    y, gm, ids, n = run_forward(pi, L, x)
+    err, flips = oracle_check(w, x, y, gm, ids, norm=cfg.rmsnorm)
+    act = gm.mean()
+    assert 0.03 < act < 0.3, act
+    del L, w
+    torch.cuda.empty_cache()
