@@ -62,6 +62,9 @@ typedef enum { PI_PRED_RELU = 0, PI_PRED_LINEAR = 1 } pi_pred_act;
 /* PI_FLAG_INPUT_RMSNORM: predictor and FFN both use x_hat = x * rsqrt(mean(x^2) + 1e-6)
  * per token (harness stand-in for the pre-FFN norm of chained stacks; reading R19). */
 #define PI_FLAG_INPUT_RMSNORM 1u
+/* PI_FLAG_MULTI_KERNEL: pi_layer_forward runs the per-step kernels (predict, compact, up,
+ * down) instead of the single fused persistent kernel (ablation / cross-check). */
+#define PI_FLAG_MULTI_KERNEL 2u
 
 #define PI_MAX_BATCH 8
 

@@ -1,11 +1,62 @@
-// fused.cuh -- single-launch persistent layer kernel (placeholder: disabled).
+// fused.cuh -- k_layer: the whole hot path of one layer in ONE
+// persistent, cooperative sm_100a kernel.
+//
+// One CTA per SM.  Warp 16 is a TMA producer: one elected lane streams every weight byte
+// the CTA needs -- its P1 rows, its block of P2 rows, then the up(/gate) and down rows of
+// its share of the active neurons -- with 1-D bulk copies (cp.async.bulk, SASS UBLKCP)
+// into an NS-stage shared-memory ring guarded by mbarriers.  Warps 0..15 (512 threads)
+// consume the ring.  Each consumer thread owns fixed 16-byte column chunks of d, so x
+// and the down-projection partial y stay in registers for the whole layer; every row dot
+// is a CTA-wide reduction (warp shuffles + one named barrier per stage).
+//
+//   phase 1  g = act_p(s * P1 x + b1)                rows of P1 dealt round-robin to CTAs
+//   -------- grid barrier 1 (g visible)
+//   phase 2  z = P2 g + b2 ; bit = z > t ; ballot     contiguous block of mask words per CTA
+//            union words + per-CTA popcount
+//   -------- grid barrier 2 (mask, union, counts visible)
+//   phase 3  every CTA prefix-sums the counts, takes compacted positions
+//            [c n / P, (c+1) n / P) -- equal work, since every compacted neuron costs the
+//            same -- extracts its ids from the union words, and streams up + down rows:
+//            h = act(s * W_up[i] x + b_up[i]) (per-token bit), y_part += h * Wd_T[i]
+//   -------- grid barrier 3 (per-CTA partials visible)
+//   phase 4  CTA c reduces its column slice over the P partials in fixed order, + b_down
+//
+// The producer runs ahead across barriers 1 and 2 for P2 rows (data-independent), so those
+// bytes stream in while the grid synchronises.  All reductions have a fixed order: the
+// result is bitwise reproducible run to run; there are no float atomics.
 #pragma once
+
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace pi {
+
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = kConsumerWarps * 32;  // 512
+constexpr int kFusedThreads = kConsumers + 32;   // + producer warp
+constexpr int kFusedMaxB = 2;
+constexpr int kMaxCP = 3;        // 16-byte chunks of d per consumer thread (d <= 12288)
+constexpr int kMaxCG = 4;        // chunks of r per lane in phase 2 (r <= 1024)
+constexpr int kMaxG = 8;         // neurons per stage
+
+constexpr int kMaxWordsP2 = 16;  // P2 words per stage
+constexpr int kRedStride = 32;   // floats per warp in the reduction buffer
+constexpr int kRedBuf = (kConsumerWarps + 1) * kRedStride;  // one reduction buffer
+
 struct FusedWork {
   bool enabled = false;
+  int P = 0, NS = 0, stage_bytes = 0, G = 0, rows_p1 = 0, words_p2 = 0, idcap = 0, smem = 0;
+  int d = 0, m = 0, r = 0;
+  unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
+  float *g = nullptr;                 // [maxB, r]
+  float *ypart = nullptr;             // [P, maxB, d]
+  int *counts = nullptr;              // [P]
+  uint32_t *mask = nullptr;           // [maxB, words]
+  uint32_t *uni = nullptr;            // [words]
 };
+
 struct FusedArgs {
   const void *w_up, *w_down, *b_up, *b_down, *p_w1, *p_b1, *p_w2, *p_b2;
   const float *x;
@@ -16,12 +67,739 @@ struct FusedArgs {
   uint32_t *mask_out;
   int32_t *ids_out, *n_out;
 };
+
+struct FusedParams {
+  const uint8_t *w_up, *w_down, *p_w1, *p_w2;
+  const void *b_up, *b_down, *p_b1, *p_b2;
+  const float *x;
+  float *y;
+  int d, m, r, words, B;
+  float t;
+  int rmsnorm, pred_relu;
+  uint32_t *mask, *uni;
+  int32_t *ids_out, *n_out;
+  float *g, *ypart;
+  int *counts;
+  unsigned long long *bar;
+  int NS, stage_bytes, G, rows_p1, words_p2, idcap;
+};
+
+// ---------------------------------------------------------------------------
+// PTX helpers: mbarrier, bulk copy, named barriers, grid barrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t a = smem_addr(bar);
+  while (true) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (done) break;
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// All P CTAs are co-resident (cooperative launch).  Monotonic 64-bit counter: an arrival
+// that returns `old` belongs to episode old / P; wait until the episode is complete.
+// A 4-second watchdog traps instead of hanging the device.
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, int P) {
+  consumers_sync();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+    const unsigned long long target = (old / (unsigned long long)P + 1ull) * (unsigned long long)P;
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_u64(bar) < target) {
+      __nanosleep(32);
+      if (globaltimer() - t0 > 4000000000ull) __trap();
+    }
+    __threadfence();
+  }
+  consumers_sync();
+}
+
+// Sum NV per-thread values over the 512 consumer threads; every consumer thread gets all NV
+// totals.  `red` is a [16 warps][kRedStride] buffer plus kRedStride totals; callers alternate
+// two buffers so the WAR hazard on reuse is covered by the next call's barrier.  Fixed order.
+template <int NV>
+__device__ __forceinline__ void cta_sum(float (&v)[NV], float *red) {
+  static_assert(NV <= kRedStride, "too many values");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[warp * kRedStride + i] = v[i];
+  }
+  consumers_sync();
+  if constexpr (NV <= 4) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) s += red[w * kRedStride + i];
+      v[i] = s;
+    }
+  } else {
+    float *tot = red + kConsumerWarps * kRedStride;
+    if (warp == 0 && lane < NV) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) s += red[w * kRedStride + lane];
+      tot[lane] = s;
+    }
+    consumers_sync();
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = tot[i];
+  }
+}
+
+template <typename T, int B, bool REGLU, int CP, int G, int RP1>
+__global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p) {
+  extern __shared__ __align__(128) uint8_t fsmem[];
+  uint8_t *smem = fsmem;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = gridDim.x, c = blockIdx.x;
+  const int d = p.d, r = p.r, m = p.m;
+  const int NS = p.NS, SB = p.stage_bytes;
+
+  // ---- shared memory carve-up ----
+  uint8_t *stages = smem;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)NS * SB);
+  uint64_t *empty = full + NS;
+  uint64_t *ids_ready = empty + NS;
+  float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][kRedBuf]
+  float *zbuf = red + 2 * kRedBuf;                                   // [B][words_p2*32]
+  float *sg = zbuf + B * kMaxWordsP2 * 32;                           // [B][r] (staging of g)
+  int *s_ids = reinterpret_cast<int *>(sg + B * 1024);               // [idcap]
+  uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
+  __shared__ float s_scale[B];
+  __shared__ int s_n, s_k0, s_k1, s_count, s_c0;
+
+  // ---- work split (identical on producer and consumer side) ----
+  const int chunks = d >> 3;
+  const int n_p1 = (r > c) ? (r - 1 - c) / P + 1 : 0;  // rows j = c + P*k
+  const int st_p1 = (n_p1 + RP1 - 1) / RP1;
+  const int w0 = (int)(((int64_t)c * p.words) / P), w1 = (int)(((int64_t)(c + 1) * p.words) / P);
+  const int st_p2 = (w1 - w0 + p.words_p2 - 1) / p.words_p2;
+  const size_t row_up = (size_t)d * 2 * (REGLU ? 2 : 1);  // bytes of one up (gate|up) row
+  const size_t row_dn = (size_t)d * 2;
+  const size_t nb = row_up + row_dn;                       // bytes per neuron in a stage
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    mbar_init(ids_ready, 1);
+    s_count = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // =====================================================================================
+  // producer warp
+  // =====================================================================================
+  if (warp == kConsumerWarps) {
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    uint32_t it = 0;
+    auto acquire = [&](uint32_t bytes) -> uint8_t * {
+      const int s = it % NS;
+      const uint32_t use = it / NS;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      mbar_expect_tx(&full[s], bytes);
+      return stages + (size_t)s * SB;
+    };
+    // phase 1: P1 rows c, c+P, ...
+    for (int st = 0; st < st_p1; ++st, ++it) {
+      const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
+      uint8_t *dst = acquire((uint32_t)(kn * row_dn));
+      const int s = it % NS;
+      for (int k = 0; k < kn; ++k) {
+        const int j = c + (k0 + k) * P;
+        bulk_g2s(dst + (size_t)k * row_dn, p.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
+      }
+    }
+    // phase 2: P2 rows of words [w0, w1) -- contiguous
+    const size_t rowb2 = (size_t)r * 2;
+    for (int st = 0; st < st_p2; ++st, ++it) {
+      const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
+      const int ra = wa * 32, rb = min(m, wb * 32);
+      const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
+      uint8_t *dst = acquire(bytes);
+      if (bytes) bulk_g2s(dst, p.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
+      else mbar_arrive(&full[it % NS]);  // (never: every word has >= 1 row) keeps phases aligned
+    }
+    // phase 3: active neurons, after the consumers published the ids
+    mbar_wait(ids_ready, 0);
+    const int n_mine = s_k1 - s_k0;
+    for (int k0 = 0; k0 < n_mine; k0 += G, ++it) {
+      const int kn = min(G, n_mine - k0);
+      uint8_t *dst = acquire((uint32_t)(kn * nb));
+      const int s = it % NS;
+      for (int k = 0; k < kn; ++k) {
+        const int i = s_ids[k0 + k];
+        bulk_g2s(dst + (size_t)k * nb, p.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
+        bulk_g2s(dst + (size_t)k * nb + row_up, p.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+      }
+    }
+    // drain: do not retire before the consumers released every stage
+    for (uint32_t j = (it > (uint32_t)NS ? it - NS : 0); j < it; ++j) mbar_wait(&empty[j % NS], (j / NS) & 1);
+    return;
+  }
+
+  // =====================================================================================
+  // consumers (512 threads)
+  // =====================================================================================
+  uint32_t it = 0;
+  int redsel = 0;
+  // x chunks in registers: chunk q of this thread = tid + 512 q
+  float xr[CP][8][B];
+#pragma unroll
+  for (int q = 0; q < CP; ++q) {
+    const int ch = tid + q * kConsumers;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (ch < chunks) {
+        float v[8];
+        ld_x8(p.x + (size_t)b * d + ch * 8, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xr[q][k][b] = v[k];
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
+      }
+    }
+  }
+  {
+    float ss[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      ss[b] = 0.f;
+#pragma unroll
+      for (int q = 0; q < CP; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ss[b] = fmaf(xr[q][k][b], xr[q][k][b], ss[b]);
+    }
+    cta_sum<B>(ss, red + (redsel++ & 1) * kRedBuf);
+#pragma unroll
+    for (int b = 0; b < B; ++b) ss[b] = p.rmsnorm ? rsqrtf(ss[b] / (float)d + 1e-6f) : 1.f;
+    if (tid < B) {
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (b == tid) s_scale[b] = ss[b];
+    }
+  }
+  float sc[B];
+  consumers_sync();
+#pragma unroll
+  for (int b = 0; b < B; ++b) sc[b] = s_scale[b];
+
+  auto wait_full = [&]() -> const uint8_t * {
+    const int s = it % NS;
+    mbar_wait(&full[s], (it / NS) & 1);
+    return stages + (size_t)s * SB;
+  };
+  auto release = [&]() {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[it % NS]);
+    ++it;
+  };
+
+  // ---------------- phase 1: g = act_p(s P1 x + b1) ----------------
+  for (int st = 0; st < st_p1; ++st) {
+    const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
+    const uint8_t *buf = wait_full();
+    float acc[RP1 * B];
+#pragma unroll
+    for (int i = 0; i < RP1 * B; ++i) acc[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < RP1; ++k) {
+      if (k < kn) {
+#pragma unroll
+        for (int q = 0; q < CP; ++q) {
+          const int ch = tid + q * kConsumers;
+          if (ch < chunks) {
+            float wf[8];
+            WT<T>::unpack(*reinterpret_cast<const Pack8 *>(buf + (size_t)k * row_dn + (size_t)ch * 16), wf);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
+          }
+        }
+      }
+    }
+    release();
+    cta_sum<RP1 * B>(acc, red + (redsel++ & 1) * kRedBuf);
+    if (tid < kn * B) {
+      const int k = tid / B, b = tid % B;
+      const int j = c + (k0 + k) * P;
+      float u = 0.f;
+#pragma unroll
+      for (int i = 0; i < RP1 * B; ++i)
+        if (i == tid) u = acc[i];
+      u = u * sc[b] + (p.p_b1 ? WT<T>::to_float(p.p_b1, j) : 0.f);
+      if (p.pred_relu) u = fmaxf(u, 0.f);
+      p.g[(size_t)b * r + j] = u;
+    }
+  }
+
+  grid_sync(p.bar, P);
+
+  // ---------------- phase 2: z = P2 g + b2, bits, union, counts ----------------
+  const int rchunks = r >> 3;
+  int lpr = 1;
+  while (lpr * 2 <= rchunks && lpr < 32) lpr *= 2;
+  const int rp = 32 / lpr, q2 = lane / lpr, sl = lane % lpr;
+  for (int i = tid; i < B * r; i += kConsumers) sg[i] = __ldcg(p.g + i);
+  consumers_sync();
+  float gr[kMaxCG][8][B];
+#pragma unroll
+  for (int q = 0; q < kMaxCG; ++q) {
+    const int ch = sl + q * lpr;
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int b = 0; b < B; ++b) gr[q][e][b] = (ch < rchunks) ? sg[b * r + ch * 8 + e] : 0.f;
+  }
+  int my_count = 0;
+  for (int st = 0; st < st_p2; ++st) {
+    const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
+    const int ra = wa * 32, nrows = min(m, wb * 32) - ra;
+    const uint8_t *buf = wait_full();
+    // rows of this stage: lane group (warp, q2) takes rows (warp*rp + q2) + k*(16*rp)
+    for (int row = warp * rp + q2; row < (wb - wa) * 32; row += kConsumerWarps * rp) {
+      float acc[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) acc[b] = 0.f;
+      if (row < nrows) {
+        const uint8_t *rowp = buf + (size_t)row * r * 2;
+#pragma unroll
+        for (int q = 0; q < kMaxCG; ++q) {
+          const int ch = sl + q * lpr;
+          if (ch < rchunks) {
+            float wf[8];
+            WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)ch * 16), wf);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[b] = fmaf(wf[e], gr[q][e][b], acc[b]);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float v = acc[b];
+        for (int o = lpr >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (sl == 0) {
+          float z = __int_as_float(0x7fc00000);
+          if (row < nrows) z = v + (p.p_b2 ? WT<T>::to_float(p.p_b2, ra + row) : 0.f);
+          zbuf[b * (kMaxWordsP2 * 32) + row] = z;
+        }
+      }
+    }
+    release();
+    consumers_sync();
+    if (warp < wb - wa) {
+      const int w = wa + warp;
+      uint32_t u = 0;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const float z = zbuf[b * (kMaxWordsP2 * 32) + warp * 32 + lane];
+        const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
+        u |= bits;
+        if (lane == 0) p.mask[(size_t)b * p.words + w] = bits;
+      }
+      if (lane == 0) {
+        p.uni[w] = u;
+        my_count += __popc(u);
+      }
+    }
+    consumers_sync();  // zbuf reuse
+  }
+  if (lane == 0 && my_count) atomicAdd(&s_count, my_count);
+  consumers_sync();
+  if (tid == 0) p.counts[c] = s_count;
+
+  grid_sync(p.bar, P);
+
+  // ---------------- phase 3: compaction of my share + sparse FFN ----------------
+  if (warp == 0) {
+    // prefix over the P per-CTA counts (CTA-block b owns words [b W/P, (b+1) W/P))
+    int run = 0, n = 0;
+    for (int base = 0; base < P; base += 32) {
+      const int b = base + lane;
+      const int v = (b < P) ? __ldcg(p.counts + b) : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      n += __shfl_sync(0xffffffffu, incl, 31);
+      (void)run;
+    }
+    const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
+    // find the first block whose cumulative count exceeds k0
+    int blk = 0, before = 0;
+    {
+      int acc = 0;
+      bool found = false;
+      for (int base = 0; base < P && !found; base += 32) {
+        const int b = base + lane;
+        const int v = (b < P) ? __ldcg(p.counts + b) : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, b < P && acc + incl > k0);
+        if (hit) {
+          const int l = __ffs(hit) - 1;
+          blk = base + l;
+          before = acc + __shfl_sync(0xffffffffu, incl - v, l);
+          found = true;
+        } else {
+          acc += __shfl_sync(0xffffffffu, incl, 31);
+        }
+      }
+      if (!found) { blk = P; before = n; }
+    }
+    // walk union words from the start of block blk; emit ids with position in [k0, k1)
+    int pos = before;
+    int w = (int)(((int64_t)blk * p.words) / P);
+    int out = 0;
+    while (pos < k1 && w < p.words) {
+      const int ww = w + lane;
+      const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
+      const int cnt = __popc(u);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      int my_pos = pos + incl - cnt;  // position of this word's first id
+      uint32_t bitsb[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
+      uint32_t v = u;
+      while (v) {
+        const int bit = __ffs(v) - 1;
+        v &= v - 1;
+        if (my_pos >= k0 && my_pos < k1) {
+          const int slot = my_pos - k0;
+          s_ids[slot] = ww * 32 + bit;
+          uint8_t tb = 0;
+#pragma unroll
+          for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
+          s_bits[slot] = tb;
+        }
+        ++my_pos;
+      }
+      pos += __shfl_sync(0xffffffffu, incl, 31);
+      w += 32;
+      (void)out;
+    }
+    if (lane == 0) {
+      s_n = n;
+      s_k0 = k0;
+      s_k1 = k1;
+    }
+  }
+  consumers_sync();
+  if (tid == 0) mbar_arrive(ids_ready);  // producer may stream the FFN rows
+  const int k0 = s_k0, n_mine = s_k1 - s_k0;
+  if (p.ids_out)
+    for (int k = tid; k < n_mine; k += kConsumers) p.ids_out[k0 + k] = s_ids[k];
+  if (p.n_out && c == 0 && tid == 0) *p.n_out = s_n;
+
+  float yr[CP][8][B];
+#pragma unroll
+  for (int q = 0; q < CP; ++q)
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+#pragma unroll
+      for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
+
+  constexpr int NA = G * B * (REGLU ? 2 : 1);
+  for (int kk = 0; kk < n_mine; kk += G) {
+    const int kn = min(G, n_mine - kk);
+    const uint8_t *buf = wait_full();
+    float acc[NA];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) acc[i] = 0.f;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (g < kn) {
+        const uint8_t *rowp = buf + (size_t)g * nb;
+#pragma unroll
+        for (int q = 0; q < CP; ++q) {
+          const int ch = tid + q * kConsumers;
+          if (ch < chunks) {
+            float wu[8];
+            if (REGLU) {
+              float wg[8];
+              WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)ch * 16), wg);
+              WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)d * 2 + (size_t)ch * 16), wu);
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+            } else {
+              WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)ch * 16), wu);
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+                acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+              }
+          }
+        }
+      }
+    }
+    cta_sum<NA>(acc, red + (redsel++ & 1) * kRedBuf);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (g < kn) {
+        const int i = s_ids[kk + g];
+        const uint8_t tb = s_bits[kk + g];
+        const float bu = p.b_up ? WT<T>::to_float(p.b_up, i) : 0.f;
+        float h[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const float a = (REGLU ? acc[(g * B + b) * 2] : acc[g * B + b]) * sc[b] + bu;
+          float hv = REGLU ? fmaxf(acc[(g * B + b) * 2 + 1] * sc[b], 0.f) * a : fmaxf(a, 0.f);
+          h[b] = ((tb >> b) & 1) ? hv : 0.f;
+        }
+        const uint8_t *dn = buf + (size_t)g * nb + row_up;
+#pragma unroll
+        for (int q = 0; q < CP; ++q) {
+          const int ch = tid + q * kConsumers;
+          if (ch < chunks) {
+            float wf[8];
+            WT<T>::unpack(*reinterpret_cast<const Pack8 *>(dn + (size_t)ch * 16), wf);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
+          }
+        }
+      }
+    }
+    release();
+  }
+  // partial y of this CTA -> global
+#pragma unroll
+  for (int q = 0; q < CP; ++q) {
+    const int ch = tid + q * kConsumers;
+    if (ch < chunks) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
+        __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
+        __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
+      }
+    }
+  }
+
+  grid_sync(p.bar, P);
+
+  // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
+  {
+    const int j0 = (int)(((int64_t)c * d) / P), j1 = (int)(((int64_t)(c + 1) * d) / P);
+    const int ncol = j1 - j0;
+    constexpr int SPL = 8;  // partial groups summed separately, then combined in order
+    float *part = reinterpret_cast<float *>(stages);  // every stage is consumed: reuse the ring
+    const int items = ncol * B;
+    for (int idx = tid; idx < items * SPL; idx += kConsumers) {
+      const int s = idx / items, it2 = idx % items;
+      const int b = it2 / ncol, j = j0 + it2 % ncol;
+      const int c0 = (s * P) / SPL, c1 = ((s + 1) * P) / SPL;
+      float acc = 0.f;
+      for (int cc = c0; cc < c1; ++cc) acc += __ldcg(p.ypart + ((size_t)cc * B + b) * d + j);
+      part[s * items + it2] = acc;
+    }
+    consumers_sync();
+    for (int it2 = tid; it2 < items; it2 += kConsumers) {
+      const int b = it2 / ncol, j = j0 + it2 % ncol;
+      float acc = 0.f;
+#pragma unroll
+      for (int s = 0; s < SPL; ++s) acc += part[s * items + it2];
+      if (p.b_down) acc += WT<T>::to_float(p.b_down, j);
+      p.y[(size_t)b * d + j] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
 template <class Alloc>
-inline bool fused_alloc(FusedWork &, int, int, int, int, int, Alloc &&) { return true; }
-inline void fused_init(FusedWork &, cudaStream_t) {}
-inline bool fused_supported(const FusedWork &w) { return w.enabled; }
+inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc) {
+  w = FusedWork{};
+  w.d = d;
+  w.m = m;
+  w.r = r;
+  const int chunks = d / 8;
+  if (chunks > kConsumers * kMaxCP || r > 8 * 32 * kMaxCG || d < 8) return true;  // unsupported: stays disabled
+  w.P = num_sms;
+  // stage size: at least one neuron (gate|up + down), one P2 word block, one P1 row; >= 32 KB
+  const size_t nb = (size_t)d * (reglu ? 6 : 4);
+  size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, (size_t)32 * r * 2});
+  sb = (sb + 127) / 128 * 128;
+  const size_t budget = 200 * 1024;
+  w.NS = (int)(budget / sb);
+  if (w.NS < 2) return true;
+  w.stage_bytes = (int)sb;
+  w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / ((size_t)32 * r * 2)));
+  w.idcap = (m + w.P - 1) / w.P + 2;
+  const size_t extra = (size_t)(2 * w.NS + 2) * 8 + (size_t)2 * kRedBuf * 4 +
+                       (size_t)kFusedMaxB * kMaxWordsP2 * 32 * 4 + (size_t)kFusedMaxB * 1024 * 4 +
+                       (size_t)w.idcap * 5 + 256;
+  w.smem = (int)((size_t)w.NS * sb + extra);
+  const int words = (m + 31) / 32;
+  if (!alloc((void **)&w.bar, 64)) return false;
+  if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
+  if (!alloc((void **)&w.ypart, (size_t)w.P * std::min(maxB, kFusedMaxB) * d * 4)) return false;
+  if (!alloc((void **)&w.counts, (size_t)w.P * 4)) return false;
+  if (!alloc((void **)&w.mask, (size_t)maxB * words * 4)) return false;
+  if (!alloc((void **)&w.uni, (size_t)words * 4)) return false;
+  w.enabled = true;
+  return true;
+}
+
+inline void fused_init(FusedWork &w, cudaStream_t s) {
+  if (w.enabled) cudaMemsetAsync(w.bar, 0, 64, s);
+}
+
+inline bool fused_supported(const FusedWork &w, int B = 1) {
+  return w.enabled && B >= 1 && B <= kFusedMaxB;
+}
+
+template <typename T, int B, bool REGLU, int CP, int G, int RP1>
+inline cudaError_t fused_launch_t(FusedWork &w, const FusedParams &prm, cudaStream_t s) {
+  auto kern = k_layer<T, B, REGLU, CP, G, RP1>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, w.smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(w.P);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = (size_t)w.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, prm);
+}
+
+// neurons per stage and P1 rows per stage, from the stage size (same rule on both sides)
+inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *G, int *RP1, int *CP) {
+  const size_t nb = (size_t)d * 2 * (reglu ? 3 : 2);
+  const int g = (int)(w.stage_bytes / nb);
+  *G = g >= 8 ? 8 : (g >= 2 ? 2 : 1);
+  *CP = (d / 8 + kConsumers - 1) / kConsumers;
+  *RP1 = (*G == 8) ? 8 : (*CP == 1 ? 4 : 2);
+}
+
 template <typename T>
-inline cudaError_t fused_launch(FusedWork &, const FusedArgs &, int, cudaStream_t) {
+inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*/, cudaStream_t s) {
+  FusedParams p{};
+  p.w_up = (const uint8_t *)a.w_up;
+  p.w_down = (const uint8_t *)a.w_down;
+  p.p_w1 = (const uint8_t *)a.p_w1;
+  p.p_w2 = (const uint8_t *)a.p_w2;
+  p.b_up = a.b_up;
+  p.b_down = a.b_down;
+  p.p_b1 = a.p_b1;
+  p.p_b2 = a.p_b2;
+  p.x = a.x;
+  p.y = a.y;
+  p.d = a.d;
+  p.m = a.m;
+  p.r = a.r;
+  p.words = a.words;
+  p.B = a.B;
+  p.t = a.threshold;
+  p.rmsnorm = a.rmsnorm;
+  p.pred_relu = a.pred_relu;
+  p.mask = a.mask_out ? a.mask_out : w.mask;
+  p.uni = w.uni;
+  p.ids_out = a.ids_out;
+  p.n_out = a.n_out;
+  p.g = w.g;
+  p.ypart = w.ypart;
+  p.counts = w.counts;
+  p.bar = w.bar;
+  p.NS = w.NS;
+  p.stage_bytes = w.stage_bytes;
+  p.rows_p1 = w.rows_p1;
+  p.words_p2 = w.words_p2;
+  p.idcap = w.idcap;
+  int G, RP1, CP;
+  fused_geometry(w, a.d, a.reglu, &G, &RP1, &CP);
+  p.G = G;
+  p.rows_p1 = RP1;
+#define PI_FL(NB, RG, CPV, GV, RV)                                                         \
+  if (a.B == NB && a.reglu == RG && CP == CPV && G == GV && RP1 == RV)                     \
+    return fused_launch_t<T, NB, RG, CPV, GV, RV>(w, p, s);
+#define PI_FL_B(NB, RG)                                                                    \
+  PI_FL(NB, RG, 1, 8, 8) PI_FL(NB, RG, 1, 2, 4) PI_FL(NB, RG, 1, 1, 4) PI_FL(NB, RG, 2, 1, 2) \
+  PI_FL(NB, RG, 3, 1, 2)
+  PI_FL_B(1, false) PI_FL_B(1, true) PI_FL_B(2, false) PI_FL_B(2, true)
+#undef PI_FL_B
+#undef PI_FL
   return cudaErrorNotSupported;
 }
+
 }  // namespace pi

@@ -102,9 +102,9 @@ __global__ void __launch_bounds__(128) k_predict2(const T *__restrict__ p2, cons
                                                    const float *__restrict__ g, float t, int m,
                                                    int r, int words, uint32_t *__restrict__ mask,
                                                    float *__restrict__ logits) {
-  extern __shared__ float smem[];
-  float *gs = smem;                       // [B][r]
-  float *zb = smem + B * r;               // [4 warps][B][32]
+  extern __shared__ float p2smem[];
+  float *gs = p2smem;                     // [B][r]
+  float *zb = p2smem + B * r;             // [4 warps][B][32]
   for (int i = threadIdx.x; i < B * r; i += blockDim.x) gs[i] = g[i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -176,7 +176,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   if (D->max_batch < 1 || D->max_batch > PI_MAX_BATCH)
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: max_batch=%d not in 1..%d", lid, D->max_batch,
                 PI_MAX_BATCH);
-  if (D->flags & ~PI_FLAG_INPUT_RMSNORM)
+  if (D->flags & ~(PI_FLAG_INPUT_RMSNORM | PI_FLAG_MULTI_KERNEL))
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: unknown flags 0x%x", lid, D->flags);
   if (std::isnan(D->logit_threshold))
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: logit_threshold is NaN", lid);
@@ -261,7 +261,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   ALLOC(L->ybuf, (size_t)MB * d * 4, false);
   ALLOC(L->hx, (size_t)MB * d * 4, false);
   ALLOC(L->hy, (size_t)MB * d * 4, false);
-  if (!fused_alloc(L->fw, d, ml, r, MB, L->num_sms, [&](void **p, size_t bytes) {
+  if (!fused_alloc(L->fw, d, ml, r, MB, L->num_sms, reglu, [&](void **p, size_t bytes) {
         return dev_alloc(L, p, bytes, false) == PI_OK;
       }))
     return cleanup(fail(PI_ERR_OUT_OF_MEMORY, "layer %d: fused workspace", lid));
@@ -338,7 +338,8 @@ extern "C" pi_status pi_layer_get_info(const pi_layer *L, pi_layer_info *info) {
   info->weight_bytes = L->weight_bytes;
   info->workspace_bytes = L->ws_bytes;
   info->launches_per_forward =
-      fused_supported(L->fw) ? 1 : 5 + ((L->flags & PI_FLAG_INPUT_RMSNORM) ? 1 : 0);
+      (!(L->flags & PI_FLAG_MULTI_KERNEL) && fused_supported(L->fw, 1)) ? 1
+                                                                        : 5 + ((L->flags & PI_FLAG_INPUT_RMSNORM) ? 1 : 0);
   return PI_OK;
 }
 
@@ -447,7 +448,7 @@ extern "C" pi_status pi_sparse_ffn(pi_layer *L, const float *x, int32_t B, const
 
 static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint32_t *mask_out,
                              int32_t *ids_out, int32_t *n_out, cudaStream_t s) {
-  if (fused_supported(L->fw)) {
+  if (!(L->flags & PI_FLAG_MULTI_KERNEL) && fused_supported(L->fw, B)) {
     return dispatch_t(L->dtype, [&](auto tt) {
       using T = typename decltype(tt)::type;
       FusedArgs a{};

@@ -29,6 +29,7 @@ PI_DT_F16, PI_DT_BF16 = 0, 1
 PI_ACT_RELU, PI_ACT_REGLU = 0, 1
 PI_PRED_RELU, PI_PRED_LINEAR = 0, 1
 PI_FLAG_INPUT_RMSNORM = 1
+PI_FLAG_MULTI_KERNEL = 2
 PI_MAX_BATCH = 8
 
 EXPORTS = ("pi_version", "pi_last_error", "pi_layer_create", "pi_layer_destroy", "pi_layer_get_info",

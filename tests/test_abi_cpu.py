@@ -103,7 +103,7 @@ def _create_status(pi, desc):
     (dict(max_batch=0), 1),
     (dict(act=1), 1),                       # ReGLU without gate
     (dict(dtype=5), 5),
-    (dict(flags=2), 1),
+    (dict(flags=4), 1),
     (dict(logit_threshold=float("nan")), 1),
     (dict(p_w2=None), 1),
 ])

@@ -217,8 +217,14 @@ def test_random_layers(env, name, dims, B):
     y, gm, ids, n = run_forward(pi, L, x)
     oracle_check(w, x, y, gm, ids, norm=cfg.rmsnorm)
     y2, gm2, ids2, n2, _ = run_steps(pi, L, x)
-    assert (gm2 == gm).all() and (ids2 == ids).all()
     oracle_check(w, x, y2, gm2, ids2, norm=cfg.rmsnorm)
+    # the fused kernel and the per-step kernels agree except on near-threshold logits
+    xo = O.rms_normalize(f(x)) if cfg.rmsnorm else f(x)
+    _, z = O.predict(xo, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), w.threshold)
+    assert ((gm2 == gm) | O.near_threshold(z, w.threshold)).all()
+    Lm = pi.Layer(w, max_batch=8, flags=flags | pi.PI_FLAG_MULTI_KERNEL)
+    y3, gm3, ids3, n3 = run_forward(pi, Lm, x)
+    assert (gm3 == gm2).all() and (y3 == y2).all()   # multi-kernel forward == the three ABI calls
 
 
 @pytest.mark.parametrize("B", [1, 2, 8])
