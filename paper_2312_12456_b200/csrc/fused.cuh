@@ -47,7 +47,8 @@ constexpr int kRedBuf = (kConsumerWarps + 1) * kRedStride;  // one reduction buf
 
 struct FusedWork {
   bool enabled = false;
-  int P = 0, NS = 0, stage_bytes = 0, G = 0, rows_p1 = 0, words_p2 = 0, idcap = 0, smem = 0;
+  int P = 0, NS = 0, stage_bytes = 0, G = 0, rows_p1 = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0;
+  unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
   int d = 0, m = 0, r = 0;
   unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
   float *g = nullptr;                 // [maxB, r]
@@ -81,7 +82,8 @@ struct FusedParams {
   float *g, *ypart;
   int *counts;
   unsigned long long *bar;
-  int NS, stage_bytes, G, rows_p1, words_p2, idcap;
+  int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap;
+  unsigned long long *trace;  // [P][16] phase timestamps (globaltimer ns) or NULL
 };
 
 // ---------------------------------------------------------------------------
@@ -210,13 +212,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)NS * SB);
   uint64_t *empty = full + NS;
   uint64_t *ids_ready = empty + NS;
+  const int wcap = p.wcap;                                           // max mask words per CTA
+  const int zst = wcap * 32;                                         // z rows per token
   float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][kRedBuf]
-  float *zbuf = red + 2 * kRedBuf;                                   // [B][words_p2*32]
-  float *sg = zbuf + B * kMaxWordsP2 * 32;                           // [B][r] (staging of g)
-  int *s_ids = reinterpret_cast<int *>(sg + B * 1024);               // [idcap]
+  float *zbuf = red + 2 * kRedBuf;                                   // [B][wcap*32]
+  float *s_b2 = zbuf + B * zst;                                      // [wcap*32]
+  float *sg = s_b2 + zst;                                            // [B][r] (staging of g)
+  float *s_bup = sg + B * 1024;                                      // [idcap]
+  int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
   __shared__ float s_scale[B];
-  __shared__ int s_n, s_k0, s_k1, s_count, s_c0;
+  __shared__ float s_b1[16];
+  __shared__ int s_n, s_k0, s_k1, s_count;
+  unsigned long long *trace = p.trace ? p.trace + (size_t)c * 16 : nullptr;
+  if (trace && tid == 0) trace[0] = globaltimer();
 
   // ---- work split (identical on producer and consumer side) ----
   const int chunks = d >> 3;
@@ -333,6 +342,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         if (b == tid) s_scale[b] = ss[b];
     }
   }
+  // biases this CTA will need, staged once (off the per-stage critical path)
+  for (int i = tid; i < (w1 - w0) * 32; i += kConsumers) {
+    const int row = w0 * 32 + i;
+    s_b2[i] = (row < m && p.p_b2) ? WT<T>::to_float(p.p_b2, row) : 0.f;
+  }
+  if (tid < n_p1) s_b1[tid] = p.p_b1 ? WT<T>::to_float(p.p_b1, c + tid * P) : 0.f;
   float sc[B];
   consumers_sync();
 #pragma unroll
@@ -382,13 +397,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 #pragma unroll
       for (int i = 0; i < RP1 * B; ++i)
         if (i == tid) u = acc[i];
-      u = u * sc[b] + (p.p_b1 ? WT<T>::to_float(p.p_b1, j) : 0.f);
+      u = u * sc[b] + s_b1[k0 + k];
       if (p.pred_relu) u = fmaxf(u, 0.f);
       p.g[(size_t)b * r + j] = u;
     }
   }
 
+  if (trace && tid == 0) trace[1] = globaltimer();
   grid_sync(p.bar, P);
+  if (trace && tid == 0) trace[2] = globaltimer();
 
   // ---------------- phase 2: z = P2 g + b2, bits, union, counts ----------------
   const int rchunks = r >> 3;
@@ -406,10 +423,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 #pragma unroll
       for (int b = 0; b < B; ++b) gr[q][e][b] = (ch < rchunks) ? sg[b * r + ch * 8 + e] : 0.f;
   }
-  int my_count = 0;
   for (int st = 0; st < st_p2; ++st) {
     const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
     const int ra = wa * 32, nrows = min(m, wb * 32) - ra;
+    const int zoff = (wa - w0) * 32;
     const uint8_t *buf = wait_full();
     // rows of this stage: lane group (warp, q2) takes rows (warp*rp + q2) + k*(16*rp)
     for (int row = warp * rp + q2; row < (wb - wa) * 32; row += kConsumerWarps * rp) {
@@ -435,116 +452,106 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       for (int b = 0; b < B; ++b) {
         float v = acc[b];
         for (int o = lpr >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (sl == 0) {
-          float z = __int_as_float(0x7fc00000);
-          if (row < nrows) z = v + (p.p_b2 ? WT<T>::to_float(p.p_b2, ra + row) : 0.f);
-          zbuf[b * (kMaxWordsP2 * 32) + row] = z;
-        }
+        if (sl == 0) zbuf[b * zst + zoff + row] = (row < nrows) ? v + s_b2[zoff + row] : __int_as_float(0x7fc00000);
       }
     }
     release();
-    consumers_sync();
-    if (warp < wb - wa) {
-      const int w = wa + warp;
-      uint32_t u = 0;
+  }
+  if (trace && tid == 0) trace[3] = globaltimer();
+  consumers_sync();
+  // ballots for all of this CTA's words: per-token mask words, union word, popcount
+  int my_count = 0;
+  for (int wl = warp; wl < w1 - w0; wl += kConsumerWarps) {
+    uint32_t u = 0;
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const float z = zbuf[b * (kMaxWordsP2 * 32) + warp * 32 + lane];
-        const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
-        u |= bits;
-        if (lane == 0) p.mask[(size_t)b * p.words + w] = bits;
-      }
-      if (lane == 0) {
-        p.uni[w] = u;
-        my_count += __popc(u);
-      }
+    for (int b = 0; b < B; ++b) {
+      const float z = zbuf[b * zst + wl * 32 + lane];
+      const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
+      u |= bits;
+      if (lane == 0) p.mask[(size_t)b * p.words + w0 + wl] = bits;
     }
-    consumers_sync();  // zbuf reuse
+    if (lane == 0) {
+      p.uni[w0 + wl] = u;
+      my_count += __popc(u);
+    }
   }
   if (lane == 0 && my_count) atomicAdd(&s_count, my_count);
   consumers_sync();
   if (tid == 0) p.counts[c] = s_count;
 
   grid_sync(p.bar, P);
+  if (trace && tid == 0) trace[4] = globaltimer();
 
   // ---------------- phase 3: compaction of my share + sparse FFN ----------------
   if (warp == 0) {
-    // prefix over the P per-CTA counts (CTA-block b owns words [b W/P, (b+1) W/P))
-    int run = 0, n = 0;
-    for (int base = 0; base < P; base += 32) {
-      const int b = base + lane;
-      const int v = (b < P) ? __ldcg(p.counts + b) : 0;
-      int incl = v;
+    // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
+    constexpr int KPL = 8;  // counts per lane (P <= 256)
+    int cv[KPL];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      n += __shfl_sync(0xffffffffu, incl, 31);
-      (void)run;
+    for (int i = 0; i < KPL; ++i) {
+      const int b = lane * KPL + i;
+      cv[i] = (b < P) ? __ldcg(p.counts + b) : 0;
     }
+    int lsum = 0;
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) lsum += cv[i];
+    int incl = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int n = __shfl_sync(0xffffffffu, incl, 31);
     const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
-    // find the first block whose cumulative count exceeds k0
-    int blk = 0, before = 0;
-    {
-      int acc = 0;
-      bool found = false;
-      for (int base = 0; base < P && !found; base += 32) {
-        const int b = base + lane;
-        const int v = (b < P) ? __ldcg(p.counts + b) : 0;
-        int incl = v;
+    if (k0 < k1) {
+      // first block whose cumulative count exceeds k0
+      int pos = incl - lsum, cand = -1, cand_before = 0;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) {
+        if (cand < 0 && pos + cv[i] > k0) {
+          cand = lane * KPL + i;
+          cand_before = pos;
+        }
+        pos += cv[i];
+      }
+      const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
+      const int src = __ffs(hit) - 1;
+      const int blk = __shfl_sync(0xffffffffu, cand, src);
+      int before = __shfl_sync(0xffffffffu, cand_before, src);
+      // walk union words from the start of block blk; keep ids with position in [k0, k1)
+      int w = (int)(((int64_t)blk * p.words) / P);
+      while (before < k1 && w < p.words) {
+        const int ww = w + lane;
+        const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
+        uint32_t bitsb[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b)
+          bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
+        const int cnt = __popc(u);
+        int wincl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
+          const int t = __shfl_up_sync(0xffffffffu, wincl, o);
+          if (lane >= o) wincl += t;
         }
-        const uint32_t hit = __ballot_sync(0xffffffffu, b < P && acc + incl > k0);
-        if (hit) {
-          const int l = __ffs(hit) - 1;
-          blk = base + l;
-          before = acc + __shfl_sync(0xffffffffu, incl - v, l);
-          found = true;
-        } else {
-          acc += __shfl_sync(0xffffffffu, incl, 31);
+        int my_pos = before + wincl - cnt;
+        uint32_t v = u;
+        while (v) {
+          const int bit = __ffs(v) - 1;
+          v &= v - 1;
+          if (my_pos >= k0 && my_pos < k1) {
+            const int slot = my_pos - k0;
+            s_ids[slot] = ww * 32 + bit;
+            uint8_t tb = 0;
+#pragma unroll
+            for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
+            s_bits[slot] = tb;
+          }
+          ++my_pos;
         }
+        before += __shfl_sync(0xffffffffu, wincl, 31);
+        w += 32;
       }
-      if (!found) { blk = P; before = n; }
-    }
-    // walk union words from the start of block blk; emit ids with position in [k0, k1)
-    int pos = before;
-    int w = (int)(((int64_t)blk * p.words) / P);
-    int out = 0;
-    while (pos < k1 && w < p.words) {
-      const int ww = w + lane;
-      const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
-      const int cnt = __popc(u);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      int my_pos = pos + incl - cnt;  // position of this word's first id
-      uint32_t bitsb[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
-      uint32_t v = u;
-      while (v) {
-        const int bit = __ffs(v) - 1;
-        v &= v - 1;
-        if (my_pos >= k0 && my_pos < k1) {
-          const int slot = my_pos - k0;
-          s_ids[slot] = ww * 32 + bit;
-          uint8_t tb = 0;
-#pragma unroll
-          for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
-          s_bits[slot] = tb;
-        }
-        ++my_pos;
-      }
-      pos += __shfl_sync(0xffffffffu, incl, 31);
-      w += 32;
-      (void)out;
     }
     if (lane == 0) {
       s_n = n;
@@ -554,10 +561,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   }
   consumers_sync();
   if (tid == 0) mbar_arrive(ids_ready);  // producer may stream the FFN rows
+  if (trace && tid == 0) trace[5] = globaltimer();
   const int k0 = s_k0, n_mine = s_k1 - s_k0;
-  if (p.ids_out)
-    for (int k = tid; k < n_mine; k += kConsumers) p.ids_out[k0 + k] = s_ids[k];
+  for (int k = tid; k < n_mine; k += kConsumers) {
+    const int i = s_ids[k];
+    s_bup[k] = p.b_up ? WT<T>::to_float(p.b_up, i) : 0.f;
+    if (p.ids_out) p.ids_out[k0 + k] = i;
+  }
   if (p.n_out && c == 0 && tid == 0) *p.n_out = s_n;
+  consumers_sync();
 
   float yr[CP][8][B];
 #pragma unroll
@@ -612,7 +624,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       if (g < kn) {
         const int i = s_ids[kk + g];
         const uint8_t tb = s_bits[kk + g];
-        const float bu = p.b_up ? WT<T>::to_float(p.b_up, i) : 0.f;
+        const float bu = s_bup[kk + g];
         float h[B];
 #pragma unroll
         for (int b = 0; b < B; ++b) {
@@ -651,33 +663,41 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     }
   }
 
+  if (trace && tid == 0) trace[6] = globaltimer();
   grid_sync(p.bar, P);
+  if (trace && tid == 0) trace[7] = globaltimer();
 
   // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
   {
     const int j0 = (int)(((int64_t)c * d) / P), j1 = (int)(((int64_t)(c + 1) * d) / P);
     const int ncol = j1 - j0;
-    constexpr int SPL = 8;  // partial groups summed separately, then combined in order
+    constexpr int SPL = 8;    // partial groups summed separately, then combined in order
+    constexpr int PPG = 32;   // partials per group (P <= 256)
     float *part = reinterpret_cast<float *>(stages);  // every stage is consumed: reuse the ring
     const int items = ncol * B;
     for (int idx = tid; idx < items * SPL; idx += kConsumers) {
-      const int s = idx / items, it2 = idx % items;
+      const int sgp = idx / items, it2 = idx % items;
       const int b = it2 / ncol, j = j0 + it2 % ncol;
-      const int c0 = (s * P) / SPL, c1 = ((s + 1) * P) / SPL;
+      const int c0 = (sgp * P) / SPL, c1 = ((sgp + 1) * P) / SPL;
+      float v[PPG];
+#pragma unroll
+      for (int q = 0; q < PPG; ++q) v[q] = (c0 + q < c1) ? __ldcg(p.ypart + ((size_t)(c0 + q) * B + b) * d + j) : 0.f;
       float acc = 0.f;
-      for (int cc = c0; cc < c1; ++cc) acc += __ldcg(p.ypart + ((size_t)cc * B + b) * d + j);
-      part[s * items + it2] = acc;
+#pragma unroll
+      for (int q = 0; q < PPG; ++q) acc += v[q];
+      part[sgp * items + it2] = acc;
     }
     consumers_sync();
     for (int it2 = tid; it2 < items; it2 += kConsumers) {
       const int b = it2 / ncol, j = j0 + it2 % ncol;
       float acc = 0.f;
 #pragma unroll
-      for (int s = 0; s < SPL; ++s) acc += part[s * items + it2];
+      for (int sgp = 0; sgp < SPL; ++sgp) acc += part[sgp * items + it2];
       if (p.b_down) acc += WT<T>::to_float(p.b_down, j);
       p.y[(size_t)b * d + j] = acc;
     }
   }
+  if (trace && tid == 0) trace[8] = globaltimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -690,7 +710,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.m = m;
   w.r = r;
   const int chunks = d / 8;
-  if (chunks > kConsumers * kMaxCP || r > 8 * 32 * kMaxCG || d < 8) return true;  // unsupported: stays disabled
+  if (chunks > kConsumers * kMaxCP || r > 8 * 32 * kMaxCG || d < 8 || r > 16 * num_sms || num_sms > 256)
+    return true;  // unsupported shape: stays disabled (per-step kernels)
   w.P = num_sms;
   // stage size: at least one neuron (gate|up + down), one P2 word block, one P1 row; >= 32 KB
   const size_t nb = (size_t)d * (reglu ? 6 : 4);
@@ -702,9 +723,11 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.stage_bytes = (int)sb;
   w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / ((size_t)32 * r * 2)));
   w.idcap = (m + w.P - 1) / w.P + 2;
+  const int words_all = (m + 31) / 32;
+  w.wcap = (words_all + w.P - 1) / w.P + 1;
   const size_t extra = (size_t)(2 * w.NS + 2) * 8 + (size_t)2 * kRedBuf * 4 +
-                       (size_t)kFusedMaxB * kMaxWordsP2 * 32 * 4 + (size_t)kFusedMaxB * 1024 * 4 +
-                       (size_t)w.idcap * 5 + 256;
+                       (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)kFusedMaxB * 1024 * 4 +
+                       (size_t)w.idcap * 9 + 256;
   w.smem = (int)((size_t)w.NS * sb + extra);
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, 64)) return false;
@@ -786,6 +809,8 @@ inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*
   p.rows_p1 = w.rows_p1;
   p.words_p2 = w.words_p2;
   p.idcap = w.idcap;
+  p.wcap = w.wcap;
+  p.trace = w.trace;
   int G, RP1, CP;
   fused_geometry(w, a.d, a.reglu, &G, &RP1, &CP);
   p.G = G;

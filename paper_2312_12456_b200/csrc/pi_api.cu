@@ -322,6 +322,13 @@ extern "C" pi_status pi_layer_destroy(pi_layer *L) {
   return PI_OK;
 }
 
+extern "C" pi_status pi_layer_set_trace(pi_layer *L, uint64_t *dev_buf) {
+  g_err.clear();
+  if (!L) return fail(PI_ERR_INVALID_ARGUMENT, "layer handle is NULL");
+  L->fw.trace = reinterpret_cast<unsigned long long *>(dev_buf);
+  return PI_OK;
+}
+
 extern "C" pi_status pi_layer_get_info(const pi_layer *L, pi_layer_info *info) {
   g_err.clear();
   if (!L || !info) return fail(PI_ERR_INVALID_ARGUMENT, "NULL argument");

@@ -34,7 +34,7 @@ PI_MAX_BATCH = 8
 
 EXPORTS = ("pi_version", "pi_last_error", "pi_layer_create", "pi_layer_destroy", "pi_layer_get_info",
            "pi_predict", "pi_compact", "pi_sparse_ffn", "pi_layer_forward", "pi_layer_forward_host",
-           "pi_stack_forward", "pi_stack_forward_host", "pi_partition")
+           "pi_stack_forward", "pi_stack_forward_host", "pi_partition", "pi_layer_set_trace")
 
 
 class PiError(RuntimeError):
@@ -83,6 +83,7 @@ def _load() -> ctypes.CDLL:
     lib.pi_stack_forward.argtypes = [P(vp), i32, vp, i32, vp, vp, vp]
     lib.pi_stack_forward_host.argtypes = [P(vp), i32, vp, i32, vp, vp]
     lib.pi_partition.argtypes = [vp, i32, i32, i32, vp, vp, vp]
+    lib.pi_layer_set_trace.argtypes = [vp, vp]
     for name in EXPORTS:
         if name not in ("pi_version", "pi_last_error"):
             getattr(lib, name).restype = ctypes.c_int
@@ -195,6 +196,10 @@ class Layer:
         assert x_host.dtype == torch.float32 and y_host.dtype == torch.float32
         _check(_lib.pi_layer_forward_host(self.handle, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
                                           _stream(stream)))
+
+    def set_trace(self, buf: Optional[torch.Tensor]):
+        """Phase timestamps of the fused kernel into buf (int64 [num_sms * 16]); None = off."""
+        _check(_lib.pi_layer_set_trace(self.handle, _ptr(buf)))
 
     # --- buffers sized for this layer ---
     def new_mask(self, B, device="cuda"):

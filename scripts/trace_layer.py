@@ -1,0 +1,61 @@
+#!/usr/bin/env python
+"""Phase timeline of the fused layer kernel (pi_layer_set_trace): per phase boundary, the
+mean and max over CTAs of (stamp - launch start), in microseconds.
+
+  python scripts/trace_layer.py [--config c4] [--reps 20] [--batch 1]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2312_12456_b200 import gen, pi  # noqa: E402
+from paper_2312_12456_b200.stack import algorithmic_bytes, build_stack  # noqa: E402
+
+NAMES = ["start", "P1 done", "grid bar 1", "P2 done", "grid bar 2", "ids ready", "FFN done", "grid bar 3", "end"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=4)
+    a = ap.parse_args()
+    cfg = gen.CONFIGS[a.config]
+    st, _ = build_stack(cfg, n_layers=min(a.layers, cfg.layers), device="cuda", max_batch=a.batch)
+    P = st.layers[0].info.num_sms
+    buf = torch.zeros(P * 16, dtype=torch.int64, device="cuda")
+    x = gen.tokens(a.batch, cfg.d, seed=3, device="cuda")
+    y = torch.empty_like(x)
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rows = []
+    for rep in range(a.reps):
+        L = st.layers[rep % len(st.layers)]
+        L.set_trace(buf)
+        buf.zero_()
+        L.forward(x, y, None, None, n)
+        torch.cuda.synchronize()
+        L.set_trace(None)
+        t = buf.view(P, 16)[:, :9].cpu().numpy().astype(np.float64)
+        t0 = t[:, 0].min()
+        rel = (t - t0) / 1e3
+        rows.append(rel)
+        x = y.clone()
+    R = np.stack(rows[2:])                    # drop warm-up reps
+    mean = R.mean(axis=(0, 1))
+    mx = R.max(axis=1).mean(axis=0)
+    nb = algorithmic_bytes(st.metas[0], int(n.item()), a.batch)
+    out = {"config": a.config, "batch": a.batch, "P": P, "bytes_per_layer": nb,
+           "phases_us_mean_over_ctas": dict(zip(NAMES, np.round(mean, 2).tolist())),
+           "phases_us_max_over_ctas": dict(zip(NAMES, np.round(mx, 2).tolist())),
+           "ideal_us_at_peak": round(nb / 6560.6e9 * 1e6, 2)}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -132,4 +132,5 @@ def test_null_handles(pi):
     assert lib.pi_layer_forward_host(None, None, 1, None, None) == 1
     assert lib.pi_stack_forward(None, 0, None, 1, None, None, None) == 1
     assert lib.pi_stack_forward_host(None, 0, None, 1, None, None) == 1
+    assert lib.pi_layer_set_trace(None, None) == 1
     assert "NULL" in lib.pi_last_error().decode()
