@@ -83,7 +83,7 @@ struct FusedParams {
   int *counts;
   unsigned long long *bar;
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap;
-  unsigned long long *trace;  // [P][16] phase timestamps (globaltimer ns) or NULL
+  unsigned long long *trace;  // [P][128] timestamps (globaltimer ns) or NULL
 };
 
 // ---------------------------------------------------------------------------
@@ -128,6 +128,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// 128-bit shared-memory load (LDS.128) from a ring stage; volatile keeps it after the mbarrier wait
+__device__ __forceinline__ Pack8 lds128(const void *p) {
+  Pack8 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.u[0]), "=r"(r.u[1]), "=r"(r.u[2]), "=r"(r.u[3])
+               : "r"(smem_addr(p)));
+  return r;
+}
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
@@ -146,18 +154,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // that returns `old` belongs to episode old / P; wait until the episode is complete.
 // A 4-second watchdog traps instead of hanging the device.
 __device__ __forceinline__ void grid_sync(unsigned long long *bar, int P) {
-  consumers_sync();
+  consumers_sync();  // every consumer thread of this CTA has issued its global writes
   if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned long long old;
-    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+    unsigned long long old, cur;
+    // release (fence + relaxed RMW), then poll with relaxed loads and acquire with a fence
+    asm volatile("fence.acq_rel.gpu;\n\tatom.add.relaxed.gpu.global.u64 %0, [%1], 1;"
+                 : "=l"(old) : "l"(bar) : "memory");
     const unsigned long long target = (old / (unsigned long long)P + 1ull) * (unsigned long long)P;
     const unsigned long long t0 = globaltimer();
-    while (ld_acquire_u64(bar) < target) {
-      __nanosleep(32);
+    while (true) {
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+      if (cur >= target) break;
       if (globaltimer() - t0 > 4000000000ull) __trap();
     }
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   consumers_sync();
 }
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   __shared__ float s_scale[B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
-  unsigned long long *trace = p.trace ? p.trace + (size_t)c * 16 : nullptr;
+  unsigned long long *trace = p.trace ? p.trace + (size_t)c * 128 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
 
   // ---- work split (identical on producer and consumer side) ----
@@ -259,6 +269,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       const int s = it % NS;
       const uint32_t use = it / NS;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      if (trace && it < 56) trace[72 + it] = globaltimer();
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
     };
@@ -356,6 +367,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   auto wait_full = [&]() -> const uint8_t * {
     const int s = it % NS;
     mbar_wait(&full[s], (it / NS) & 1);
+    if (trace && tid == 0 && it < 56) trace[16 + it] = globaltimer();
     return stages + (size_t)s * SB;
   };
   auto release = [&]() {
@@ -379,7 +391,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           const int ch = tid + q * kConsumers;
           if (ch < chunks) {
             float wf[8];
-            WT<T>::unpack(*reinterpret_cast<const Pack8 *>(buf + (size_t)k * row_dn + (size_t)ch * 16), wf);
+            WT<T>::unpack(lds128(buf + (size_t)k * row_dn + (size_t)ch * 16), wf);
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -440,7 +452,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           const int ch = sl + q * lpr;
           if (ch < rchunks) {
             float wf[8];
-            WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)ch * 16), wf);
+            WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wf);
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -597,15 +609,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
             float wu[8];
             if (REGLU) {
               float wg[8];
-              WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)ch * 16), wg);
-              WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)d * 2 + (size_t)ch * 16), wu);
+              WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wg);
+              WT<T>::unpack(lds128(rowp + (size_t)d * 2 + (size_t)ch * 16), wu);
 #pragma unroll
               for (int b = 0; b < B; ++b)
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
                   acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
             } else {
-              WT<T>::unpack(*reinterpret_cast<const Pack8 *>(rowp + (size_t)ch * 16), wu);
+              WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wu);
             }
 #pragma unroll
             for (int b = 0; b < B; ++b)
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           const int ch = tid + q * kConsumers;
           if (ch < chunks) {
             float wf[8];
-            WT<T>::unpack(*reinterpret_cast<const Pack8 *>(dn + (size_t)ch * 16), wf);
+            WT<T>::unpack(lds128(dn + (size_t)ch * 16), wf);
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll

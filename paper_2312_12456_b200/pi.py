@@ -198,7 +198,7 @@ class Layer:
                                           _stream(stream)))
 
     def set_trace(self, buf: Optional[torch.Tensor]):
-        """Phase timestamps of the fused kernel into buf (int64 [num_sms * 16]); None = off."""
+        """Phase timestamps of the fused kernel into buf (int64 [num_sms * 128]); None = off."""
         _check(_lib.pi_layer_set_trace(self.handle, _ptr(buf)))
 
     # --- buffers sized for this layer ---
