@@ -1,13 +1,20 @@
 // fused.cuh -- k_layer: the whole hot path of one layer in ONE
 // persistent, cooperative sm_100a kernel.
 //
-// One CTA per SM.  Warp 16 is a TMA producer: one elected lane streams every weight byte
-// the CTA needs -- its P1 rows, its block of P2 rows, then the up(/gate) and down rows of
-// its share of the active neurons -- with 1-D bulk copies (cp.async.bulk, SASS UBLKCP)
-// into an NS-stage shared-memory ring guarded by mbarriers.  Warps 0..15 (512 threads)
-// consume the ring.  Each consumer thread owns fixed 16-byte column chunks of d, so x
-// and the down-projection partial y stay in registers for the whole layer; every row dot
-// is a CTA-wide reduction (warp shuffles + one named barrier per stage).
+// One CTA per SM, 17 warps in three roles:
+//   producer (warp 16) -- one elected lane streams every weight byte the CTA needs (its P1
+//       rows, its block of P2 rows, then the up(/gate) and down rows of its share of the
+//       active neurons) with 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) into an
+//       NS-stage shared-memory ring guarded by full/empty mbarriers;
+//   up group (warps 0..7, 256 threads) -- owns x in registers (fixed 16-byte column chunks
+//       of d per thread); computes the P1 row dots and, per ring stage, the up (and gate)
+//       dots of the stage's neurons: per-warp transpose reductions, one 256-thread named
+//       barrier per stage, then h = act(.) is handed to the down group through shared
+//       memory and an "h ready" mbarrier;
+//   down group (warps 8..15, 256 threads) -- computes the P2 GEMV + threshold + ballot
+//       (one warp per ring stage of mask words, transpose-reduced), then, per FFN stage,
+//       accumulates h * down-row into its register-resident partial y.
+// The two groups are decoupled by the ring: the up group runs ahead of the down group.
 //
 //   phase 1  g = act_p(s * P1 x + b1)                rows of P1 dealt round-robin to CTAs
 //   -------- grid barrier 1 (g visible)
@@ -33,29 +40,29 @@
 
 namespace pi {
 
-constexpr int kConsumerWarps = 16;
-constexpr int kConsumers = kConsumerWarps * 32;  // 512
-constexpr int kFusedThreads = kConsumers + 32;   // + producer warp
+constexpr int kGroupWarps = 8;                        // warps per group (up / down)
+constexpr int kGroup = kGroupWarps * 32;              // 256 threads per group
+constexpr int kConsumerWarps = 2 * kGroupWarps;       // 16
+constexpr int kConsumers = kConsumerWarps * 32;       // 512
+constexpr int kFusedThreads = kConsumers + 32;        // + producer warp
 constexpr int kFusedMaxB = 2;
-constexpr int kMaxCP = 3;        // 16-byte chunks of d per consumer thread (d <= 12288)
-constexpr int kMaxCG = 4;        // chunks of r per lane in phase 2 (r <= 1024)
-constexpr int kMaxG = 8;         // neurons per stage
-
-constexpr int kMaxWordsP2 = 16;  // P2 words per stage
-constexpr int kRedStride = 32;   // floats per warp in the reduction buffer
-constexpr int kRedBuf = (kConsumerWarps + 1) * kRedStride;  // one reduction buffer
+constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 16384)
+constexpr int kMaxCG = 4;        // 16-byte chunks of r per lane in phase 2 (r <= 1024)
+constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
+constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
 
 struct FusedWork {
   bool enabled = false;
-  int P = 0, NS = 0, stage_bytes = 0, G = 0, rows_p1 = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0;
-  unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
+  int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0;
   int d = 0, m = 0, r = 0;
+  bool reglu = false;
   unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
   float *g = nullptr;                 // [maxB, r]
   float *ypart = nullptr;             // [P, maxB, d]
   int *counts = nullptr;              // [P]
   uint32_t *mask = nullptr;           // [maxB, words]
   uint32_t *uni = nullptr;            // [words]
+  unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
 };
 
 struct FusedArgs {
@@ -98,6 +105,10 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
@@ -139,11 +150,7 @@ __device__ __forceinline__ Pack8 lds128(const void *p) {
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
+__device__ __forceinline__ void up_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kGroup) : "memory"); }
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -172,66 +179,83 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, int P) {
   consumers_sync();
 }
 
-// Sum NV per-thread values over the 512 consumer threads; every consumer thread gets all NV
-// totals.  `red` is a [16 warps][kRedStride] buffer plus kRedStride totals; callers alternate
-// two buffers so the WAR hazard on reuse is covered by the next call's barrier.  Fixed order.
+// Transpose reduction of NV per-lane partials (NV a power of two <= 32): afterwards every
+// lane l holds the warp-wide total of value (l & (NV - 1)).  NV - 1 + log2(32 / NV) shuffles
+// instead of 5 NV.  Fixed order.
 template <int NV>
-__device__ __forceinline__ void cta_sum(float (&v)[NV], float *red) {
-  static_assert(NV <= kRedStride, "too many values");
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ float warp_reduce_multi(float (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
-  if (lane == 0) {
+  for (int s = NV / 2; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
 #pragma unroll
-    for (int i = 0; i < NV; ++i) red[warp * kRedStride + i] = v[i];
-  }
-  consumers_sync();
-  if constexpr (NV <= 4) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) s += red[w * kRedStride + i];
-      v[i] = s;
+    for (int i = 0; i < s; ++i) {
+      const float send = up ? v[i] : v[i + s];
+      const float keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
     }
-  } else {
-    float *tot = red + kConsumerWarps * kRedStride;
-    if (warp == 0 && lane < NV) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < kConsumerWarps; ++w) s += red[w * kRedStride + lane];
-      tot[lane] = s;
-    }
-    consumers_sync();
-#pragma unroll
-    for (int i = 0; i < NV; ++i) v[i] = tot[i];
   }
+  float r = v[0];
+#pragma unroll
+  for (int o = NV; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
 }
 
-template <typename T, int B, bool REGLU, int CP, int G, int RP1>
+template <int N>
+struct Pow2Ceil {
+  static constexpr int v = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+};
+
+// Up-group reduction of NV values (NV <= 32): per-warp transpose reduction, lanes < NV write
+// red[warp][l]; after the 256-thread barrier, red holds 8 partials per value.
+template <int NV>
+__device__ __forceinline__ void up_partials(float (&v)[NV], float *red) {
+  constexpr int NP = Pow2Ceil<NV>::v;
+  float w[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) w[i] = (i < NV) ? v[i] : 0.f;
+  const float r = warp_reduce_multi<NP>(w);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane < NV) red[warp * kRedStride + lane] = r;
+  up_sync();
+}
+__device__ __forceinline__ float up_total(const float *red, int i) {
+  float s = 0.f;
+#pragma unroll
+  for (int w = 0; w < kGroupWarps; ++w) s += red[w * kRedStride + i];
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// the kernel
+//   CH : 16-byte chunks of d per group thread (chunk = t + 256 q, q < CH)
+//   NA : max neurons per ring stage (also bounds P1 rows per stage: NA == 1 -> 2, else 8)
+// ---------------------------------------------------------------------------
+template <typename T, int B, bool REGLU, int CH, int NA>
 __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p) {
+  constexpr int RPM = (NA == 1) ? 2 : 8;      // max P1 rows per stage
+  constexpr int RW = (B == 1) ? 16 : 8;       // P2 rows per transpose reduction
   extern __shared__ __align__(128) uint8_t fsmem[];
   uint8_t *smem = fsmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = gridDim.x, c = blockIdx.x;
   const int d = p.d, r = p.r, m = p.m;
-  const int NS = p.NS, SB = p.stage_bytes;
+  const int NS = p.NS, SB = p.stage_bytes, G = p.G, RP1 = p.rows_p1;
 
   // ---- shared memory carve-up ----
   uint8_t *stages = smem;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)NS * SB);
   uint64_t *empty = full + NS;
-  uint64_t *ids_ready = empty + NS;
-  const int wcap = p.wcap;                                           // max mask words per CTA
-  const int zst = wcap * 32;                                         // z rows per token
-  float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][kRedBuf]
-  float *zbuf = red + 2 * kRedBuf;                                   // [B][wcap*32]
-  float *s_b2 = zbuf + B * zst;                                      // [wcap*32]
-  float *sg = s_b2 + zst;                                            // [B][r] (staging of g)
-  float *s_bup = sg + B * 1024;                                      // [idcap]
+  uint64_t *hready = empty + NS;
+  uint64_t *ids_ready = hready + NS;
+  float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][8][32]
+  float *hs = red + 2 * kGroupWarps * kRedStride;                    // [NS][NA*B]
+  float *s_b2 = hs + NS * NA * B;                                    // [wcap*32]
+  float *s_bup = s_b2 + p.wcap * 32;                                 // [idcap]
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
   __shared__ float s_scale[B];
+  __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
   unsigned long long *trace = p.trace ? p.trace + (size_t)c * 128 : nullptr;
@@ -250,7 +274,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], kGroupWarps);
+      mbar_init(&hready[s], 1);
     }
     mbar_init(ids_ready, 1);
     s_count = 0;
@@ -273,8 +298,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
     };
-    // phase 1: P1 rows c, c+P, ...
-    for (int st = 0; st < st_p1; ++st, ++it) {
+    for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
       const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
       uint8_t *dst = acquire((uint32_t)(kn * row_dn));
       const int s = it % NS;
@@ -283,18 +307,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         bulk_g2s(dst + (size_t)k * row_dn, p.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
       }
     }
-    // phase 2: P2 rows of words [w0, w1) -- contiguous
     const size_t rowb2 = (size_t)r * 2;
-    for (int st = 0; st < st_p2; ++st, ++it) {
+    for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 rows of words [w0, w1), contiguous
       const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
       const int ra = wa * 32, rb = min(m, wb * 32);
       const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
       uint8_t *dst = acquire(bytes);
-      if (bytes) bulk_g2s(dst, p.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
-      else mbar_arrive(&full[it % NS]);  // (never: every word has >= 1 row) keeps phases aligned
+      bulk_g2s(dst, p.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
     }
-    // phase 3: active neurons, after the consumers published the ids
-    mbar_wait(ids_ready, 0);
+    mbar_wait(ids_ready, 0);                     // phase 3: after the ids are published
     const int n_mine = s_k1 - s_k0;
     for (int k0 = 0; k0 < n_mine; k0 += G, ++it) {
       const int kn = min(G, n_mine - k0);
@@ -312,189 +333,196 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   }
 
   // =====================================================================================
-  // consumers (512 threads)
+  // consumers
   // =====================================================================================
-  uint32_t it = 0;
-  int redsel = 0;
-  // x chunks in registers: chunk q of this thread = tid + 512 q
-  float xr[CP][8][B];
-#pragma unroll
-  for (int q = 0; q < CP; ++q) {
-    const int ch = tid + q * kConsumers;
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (ch < chunks) {
-        float v[8];
-        ld_x8(p.x + (size_t)b * d + ch * 8, v);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) xr[q][k][b] = v[k];
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
-      }
-    }
-  }
-  {
-    float ss[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      ss[b] = 0.f;
-#pragma unroll
-      for (int q = 0; q < CP; ++q)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) ss[b] = fmaf(xr[q][k][b], xr[q][k][b], ss[b]);
-    }
-    cta_sum<B>(ss, red + (redsel++ & 1) * kRedBuf);
-#pragma unroll
-    for (int b = 0; b < B; ++b) ss[b] = p.rmsnorm ? rsqrtf(ss[b] / (float)d + 1e-6f) : 1.f;
-    if (tid < B) {
-#pragma unroll
-      for (int b = 0; b < B; ++b)
-        if (b == tid) s_scale[b] = ss[b];
-    }
-  }
-  // biases this CTA will need, staged once (off the per-stage critical path)
-  for (int i = tid; i < (w1 - w0) * 32; i += kConsumers) {
-    const int row = w0 * 32 + i;
-    s_b2[i] = (row < m && p.p_b2) ? WT<T>::to_float(p.p_b2, row) : 0.f;
-  }
-  if (tid < n_p1) s_b1[tid] = p.p_b1 ? WT<T>::to_float(p.p_b1, c + tid * P) : 0.f;
-  float sc[B];
-  consumers_sync();
-#pragma unroll
-  for (int b = 0; b < B; ++b) sc[b] = s_scale[b];
-
-  auto wait_full = [&]() -> const uint8_t * {
-    const int s = it % NS;
-    mbar_wait(&full[s], (it / NS) & 1);
+  const bool is_up = warp < kGroupWarps;
+  const int gt = is_up ? tid : tid - kGroup;   // thread index inside its group
+  const int gw = gt >> 5;                      // warp index inside its group
+  auto stage_ptr = [&](uint32_t it) { return stages + (size_t)(it % NS) * SB; };
+  auto wait_full = [&](uint32_t it) {
+    mbar_wait(&full[it % NS], (it / NS) & 1);
     if (trace && tid == 0 && it < 56) trace[16 + it] = globaltimer();
-    return stages + (size_t)s * SB;
-  };
-  auto release = [&]() {
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[it % NS]);
-    ++it;
   };
 
-  // ---------------- phase 1: g = act_p(s P1 x + b1) ----------------
-  for (int st = 0; st < st_p1; ++st) {
-    const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
-    const uint8_t *buf = wait_full();
-    float acc[RP1 * B];
+  float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
+  float sc[B];
+  if (is_up) {
 #pragma unroll
-    for (int i = 0; i < RP1 * B; ++i) acc[i] = 0.f;
+    for (int q = 0; q < CH; ++q) {
+      const int ch = gt + q * kGroup;
 #pragma unroll
-    for (int k = 0; k < RP1; ++k) {
-      if (k < kn) {
+      for (int b = 0; b < B; ++b) {
+        if (ch < chunks) {
+          float v[8];
+          ld_x8(p.x + (size_t)b * d + ch * 8, v);
 #pragma unroll
-        for (int q = 0; q < CP; ++q) {
-          const int ch = tid + q * kConsumers;
-          if (ch < chunks) {
-            float wf[8];
-            WT<T>::unpack(lds128(buf + (size_t)k * row_dn + (size_t)ch * 16), wf);
+          for (int k = 0; k < 8; ++k) xr[q][k][b] = v[k];
+        } else {
 #pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
-          }
+          for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
         }
       }
     }
-    release();
-    cta_sum<RP1 * B>(acc, red + (redsel++ & 1) * kRedBuf);
-    if (tid < kn * B) {
-      const int k = tid / B, b = tid % B;
-      const int j = c + (k0 + k) * P;
-      float u = 0.f;
 #pragma unroll
-      for (int i = 0; i < RP1 * B; ++i)
-        if (i == tid) u = acc[i];
-      u = u * sc[b] + s_b1[k0 + k];
-      if (p.pred_relu) u = fmaxf(u, 0.f);
-      p.g[(size_t)b * r + j] = u;
+    for (int b = 0; b < B; ++b) {
+      float ss = 0.f;
+#pragma unroll
+      for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ss = fmaf(xr[q][k][b], xr[q][k][b], ss);
+      ss = warp_sum(ss);
+      if (lane == 0) s_ss[gw][b] = ss;
+    }
+    if (gt < n_p1) s_b1[gt] = p.p_b1 ? WT<T>::to_float(p.p_b1, c + gt * P) : 0.f;
+    up_sync();
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float ss = 0.f;
+#pragma unroll
+      for (int w = 0; w < kGroupWarps; ++w) ss += s_ss[w][b];
+      sc[b] = p.rmsnorm ? rsqrtf(ss / (float)d + 1e-6f) : 1.f;
+    }
+  } else {
+    // down group: stage this CTA's b2 slice (off the per-stage critical path)
+    for (int i = gt; i < (w1 - w0) * 32; i += kGroup) {
+      const int row = w0 * 32 + i;
+      s_b2[i] = (row < m && p.p_b2) ? WT<T>::to_float(p.p_b2, row) : 0.f;
     }
   }
 
+  // ---------------- phase 1 (up group): g = act_p(s P1 x + b1) ----------------
+  if (is_up) {
+    for (int st = 0; st < st_p1; ++st) {
+      const uint32_t it = st;
+      const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
+      wait_full(it);
+      const uint8_t *buf = stage_ptr(it);
+      float acc[RPM * B];
+#pragma unroll
+      for (int i = 0; i < RPM * B; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int k = 0; k < RPM; ++k) {
+        if (k < kn) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            if (ch < chunks) {
+              float wf[8];
+              WT<T>::unpack(lds128(buf + (size_t)k * row_dn + (size_t)ch * 16), wf);
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
+            }
+          }
+        }
+      }
+      float *rb = red + (it & 1) * kGroupWarps * kRedStride;
+      up_partials<RPM * B>(acc, rb);
+      if (gt == 0) mbar_arrive_cnt(&empty[it % NS], kGroupWarps);  // every up warp has read the stage
+      if (gt < kn * B) {
+        const int k = gt / B, b = gt % B;
+        const int j = c + (k0 + k) * P;
+        float u = up_total(rb, gt) * sc[b] + s_b1[k0 + k];
+        if (p.pred_relu) u = fmaxf(u, 0.f);
+        p.g[(size_t)b * r + j] = u;
+      }
+    }
+  }
   if (trace && tid == 0) trace[1] = globaltimer();
   grid_sync(p.bar, P);
   if (trace && tid == 0) trace[2] = globaltimer();
 
-  // ---------------- phase 2: z = P2 g + b2, bits, union, counts ----------------
-  const int rchunks = r >> 3;
-  int lpr = 1;
-  while (lpr * 2 <= rchunks && lpr < 32) lpr *= 2;
-  const int rp = 32 / lpr, q2 = lane / lpr, sl = lane % lpr;
-  for (int i = tid; i < B * r; i += kConsumers) sg[i] = __ldcg(p.g + i);
-  consumers_sync();
-  float gr[kMaxCG][8][B];
+  // ---------------- phase 2 (down group): z = P2 g + b2, bits, union, counts ----------------
+  if (!is_up) {
+    const int rchunks = r >> 3;
+    float gr[kMaxCG][8][B];
 #pragma unroll
-  for (int q = 0; q < kMaxCG; ++q) {
-    const int ch = sl + q * lpr;
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-#pragma unroll
-      for (int b = 0; b < B; ++b) gr[q][e][b] = (ch < rchunks) ? sg[b * r + ch * 8 + e] : 0.f;
-  }
-  for (int st = 0; st < st_p2; ++st) {
-    const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
-    const int ra = wa * 32, nrows = min(m, wb * 32) - ra;
-    const int zoff = (wa - w0) * 32;
-    const uint8_t *buf = wait_full();
-    // rows of this stage: lane group (warp, q2) takes rows (warp*rp + q2) + k*(16*rp)
-    for (int row = warp * rp + q2; row < (wb - wa) * 32; row += kConsumerWarps * rp) {
-      float acc[B];
-#pragma unroll
-      for (int b = 0; b < B; ++b) acc[b] = 0.f;
-      if (row < nrows) {
-        const uint8_t *rowp = buf + (size_t)row * r * 2;
-#pragma unroll
-        for (int q = 0; q < kMaxCG; ++q) {
-          const int ch = sl + q * lpr;
-          if (ch < rchunks) {
-            float wf[8];
-            WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wf);
-#pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc[b] = fmaf(wf[e], gr[q][e][b], acc[b]);
-          }
-        }
-      }
+    for (int q = 0; q < kMaxCG; ++q) {
+      const int ch = lane + q * 32;
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        float v = acc[b];
-        for (int o = lpr >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (sl == 0) zbuf[b * zst + zoff + row] = (row < nrows) ? v + s_b2[zoff + row] : __int_as_float(0x7fc00000);
+        if (ch < rchunks) {
+          const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(p.g + (size_t)b * r + ch * 8));
+          const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(p.g + (size_t)b * r + ch * 8) + 1);
+          gr[q][0][b] = a0.x; gr[q][1][b] = a0.y; gr[q][2][b] = a0.z; gr[q][3][b] = a0.w;
+          gr[q][4][b] = a1.x; gr[q][5][b] = a1.y; gr[q][6][b] = a1.z; gr[q][7][b] = a1.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) gr[q][e][b] = 0.f;
+        }
       }
     }
-    release();
+    int my_count = 0;
+    for (int st = gw; st < st_p2; st += kGroupWarps) {
+      const uint32_t it = st_p1 + st;
+      const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
+      const int nrows = min(m, wb * 32) - wa * 32;
+      wait_full(it);
+      const uint8_t *buf = stage_ptr(it);
+      for (int wl = 0; wl < wb - wa; ++wl) {
+        float zfin[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) zfin[b] = 0.f;
+#pragma unroll
+        for (int q = 0; q < 32 / RW; ++q) {
+          float v[B][RW];
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+#pragma unroll
+            for (int i = 0; i < RW; ++i) v[b][i] = 0.f;
+#pragma unroll
+          for (int i = 0; i < RW; ++i) {
+            const int row = wl * 32 + q * RW + i;
+            if (row < nrows) {
+              const uint8_t *rowp = buf + (size_t)row * r * 2;
+#pragma unroll
+              for (int cq = 0; cq < kMaxCG; ++cq) {
+                const int ch = lane + cq * 32;
+                if (ch < rchunks) {
+                  float wf[8];
+                  WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wf);
+#pragma unroll
+                  for (int b = 0; b < B; ++b)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) v[b][i] = fmaf(wf[e], gr[cq][e][b], v[b][i]);
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            const float z = warp_reduce_multi<RW>(v[b]);
+            if (lane / RW == q) zfin[b] = z;      // lane l ends up holding row l of the word
+          }
+        }
+        const int rl = wl * 32 + lane;            // row of this lane, stage-local
+        const int zoff = (wa - w0) * 32;
+        uint32_t u = 0;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          const float z = (rl < nrows) ? zfin[b] + s_b2[zoff + rl] : __int_as_float(0x7fc00000);
+          const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
+          u |= bits;
+          if (lane == 0) p.mask[(size_t)b * p.words + wa + wl] = bits;
+        }
+        if (lane == 0) {
+          p.uni[wa + wl] = u;
+          my_count += __popc(u);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cnt(&empty[it % NS], kGroupWarps);
+    }
+    if (lane == 0 && my_count) atomicAdd(&s_count, my_count);
   }
   if (trace && tid == 0) trace[3] = globaltimer();
   consumers_sync();
-  // ballots for all of this CTA's words: per-token mask words, union word, popcount
-  int my_count = 0;
-  for (int wl = warp; wl < w1 - w0; wl += kConsumerWarps) {
-    uint32_t u = 0;
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const float z = zbuf[b * zst + wl * 32 + lane];
-      const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
-      u |= bits;
-      if (lane == 0) p.mask[(size_t)b * p.words + w0 + wl] = bits;
-    }
-    if (lane == 0) {
-      p.uni[w0 + wl] = u;
-      my_count += __popc(u);
-    }
-  }
-  if (lane == 0 && my_count) atomicAdd(&s_count, my_count);
-  consumers_sync();
   if (tid == 0) p.counts[c] = s_count;
-
   grid_sync(p.bar, P);
   if (trace && tid == 0) trace[4] = globaltimer();
 
-  // ---------------- phase 3: compaction of my share + sparse FFN ----------------
+  // ---------------- phase 3: compaction of my share ----------------
   if (warp == 0) {
     // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
     constexpr int KPL = 8;  // counts per lane (P <= 256)
@@ -516,7 +544,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     const int n = __shfl_sync(0xffffffffu, incl, 31);
     const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
     if (k0 < k1) {
-      // first block whose cumulative count exceeds k0
       int pos = incl - lsum, cand = -1, cand_before = 0;
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
@@ -583,94 +610,115 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   if (p.n_out && c == 0 && tid == 0) *p.n_out = s_n;
   consumers_sync();
 
-  float yr[CP][8][B];
+  // ---------------- phase 3: the sparse FFN ----------------
+  const uint32_t it_ffn = st_p1 + st_p2;
+  const int n_st = (n_mine + G - 1) / G;
+  if (is_up) {
+    constexpr int NV = NA * B * (REGLU ? 2 : 1);
+    for (int f = 0; f < n_st; ++f) {
+      const uint32_t it = it_ffn + f;
+      const int kk = f * G, kn = min(G, n_mine - kk);
+      wait_full(it);
+      const uint8_t *buf = stage_ptr(it);
+      float acc[NV];
 #pragma unroll
-  for (int q = 0; q < CP; ++q)
+      for (int i = 0; i < NV; ++i) acc[i] = 0.f;
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
+      for (int g = 0; g < NA; ++g) {
+        if (g < kn) {
+          const uint8_t *rowp = buf + (size_t)g * nb;
 #pragma unroll
-      for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
-
-  constexpr int NA = G * B * (REGLU ? 2 : 1);
-  for (int kk = 0; kk < n_mine; kk += G) {
-    const int kn = min(G, n_mine - kk);
-    const uint8_t *buf = wait_full();
-    float acc[NA];
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            if (ch < chunks) {
+              float wu[8];
+              if (REGLU) {
+                float wg[8];
+                WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wg);
+                WT<T>::unpack(lds128(rowp + (size_t)d * 2 + (size_t)ch * 16), wu);
 #pragma unroll
-    for (int i = 0; i < NA; ++i) acc[i] = 0.f;
+                for (int b = 0; b < B; ++b)
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (g < kn) {
-        const uint8_t *rowp = buf + (size_t)g * nb;
-#pragma unroll
-        for (int q = 0; q < CP; ++q) {
-          const int ch = tid + q * kConsumers;
-          if (ch < chunks) {
-            float wu[8];
-            if (REGLU) {
-              float wg[8];
-              WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wg);
-              WT<T>::unpack(lds128(rowp + (size_t)d * 2 + (size_t)ch * 16), wu);
+                  for (int e = 0; e < 8; ++e)
+                    acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+              } else {
+                WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wu);
+              }
 #pragma unroll
               for (int b = 0; b < B; ++b)
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
-            } else {
-              WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wu);
+                for (int e = 0; e < 8; ++e) {
+                  const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+                  acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+                }
             }
-#pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-                acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
-              }
           }
         }
       }
+      float *rb = red + (f & 1) * kGroupWarps * kRedStride;
+      up_partials<NV>(acc, rb);
+      if (warp == 0) {
+        if (lane < kn * B) {
+          const int g = lane / B, b = lane % B;
+          const int slot = kk + g;
+          const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + s_bup[slot];
+          float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
+          hs[(it % NS) * (NA * B) + lane] = ((s_bits[slot] >> b) & 1) ? hv : 0.f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hready[it % NS]);
+      }
     }
-    cta_sum<NA>(acc, red + (redsel++ & 1) * kRedBuf);
+  } else {
+    float yr[CH][8][B];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (g < kn) {
-        const int i = s_ids[kk + g];
-        const uint8_t tb = s_bits[kk + g];
-        const float bu = s_bup[kk + g];
-        float h[B];
+    for (int q = 0; q < CH; ++q)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
+    for (int f = 0; f < n_st; ++f) {
+      const uint32_t it = it_ffn + f;
+      const int kn = min(G, n_mine - f * G);
+      wait_full(it);
+      mbar_wait(&hready[it % NS], (f / NS) & 1);
+      const uint8_t *buf = stage_ptr(it);
+      const float *hh = hs + (it % NS) * (NA * B);
+#pragma unroll
+      for (int g = 0; g < NA; ++g) {
+        if (g < kn) {
+          float h[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) h[b] = hh[g * B + b];
+          const uint8_t *dn = buf + (size_t)g * nb + row_up;
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            if (ch < chunks) {
+              float wf[8];
+              WT<T>::unpack(lds128(dn + (size_t)ch * 16), wf);
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[it % NS]);
+    }
+    // partial y of this CTA -> global
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const int ch = gt + q * kGroup;
+      if (ch < chunks) {
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-          const float a = (REGLU ? acc[(g * B + b) * 2] : acc[g * B + b]) * sc[b] + bu;
-          float hv = REGLU ? fmaxf(acc[(g * B + b) * 2 + 1] * sc[b], 0.f) * a : fmaxf(a, 0.f);
-          h[b] = ((tb >> b) & 1) ? hv : 0.f;
+          float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
+          __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
+          __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
         }
-        const uint8_t *dn = buf + (size_t)g * nb + row_up;
-#pragma unroll
-        for (int q = 0; q < CP; ++q) {
-          const int ch = tid + q * kConsumers;
-          if (ch < chunks) {
-            float wf[8];
-            WT<T>::unpack(lds128(dn + (size_t)ch * 16), wf);
-#pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
-          }
-        }
-      }
-    }
-    release();
-  }
-  // partial y of this CTA -> global
-#pragma unroll
-  for (int q = 0; q < CP; ++q) {
-    const int ch = tid + q * kConsumers;
-    if (ch < chunks) {
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
-        __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
-        __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
       }
     }
   }
@@ -715,17 +763,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+inline int fused_ch(int d) { return (d / 8 + kGroup - 1) / kGroup; }
+
 template <class Alloc>
 inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc) {
   w = FusedWork{};
   w.d = d;
   w.m = m;
   w.r = r;
-  const int chunks = d / 8;
-  if (chunks > kConsumers * kMaxCP || r > 8 * 32 * kMaxCG || d < 8 || r > 16 * num_sms || num_sms > 256)
+  w.reglu = reglu;
+  const int ch = fused_ch(d);
+  if (ch > kMaxCH || ch == 5 || ch == 7 || r > 8 * 32 * kMaxCG || d < 8 || r > 16 * num_sms || num_sms > 256)
     return true;  // unsupported shape: stays disabled (per-step kernels)
   w.P = num_sms;
-  // stage size: at least one neuron (gate|up + down), one P2 word block, one P1 row; >= 32 KB
+  // stage: >= one neuron (gate|up + down), one P2 word block, >= 32 KB
   const size_t nb = (size_t)d * (reglu ? 6 : 4);
   size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, (size_t)32 * r * 2});
   sb = (sb + 127) / 128 * 128;
@@ -737,9 +788,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.idcap = (m + w.P - 1) / w.P + 2;
   const int words_all = (m + 31) / 32;
   w.wcap = (words_all + w.P - 1) / w.P + 1;
-  const size_t extra = (size_t)(2 * w.NS + 2) * 8 + (size_t)2 * kRedBuf * 4 +
-                       (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)kFusedMaxB * 1024 * 4 +
-                       (size_t)w.idcap * 9 + 256;
+  const size_t extra = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
+                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 256;
   w.smem = (int)((size_t)w.NS * sb + extra);
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, 64)) return false;
@@ -756,13 +806,30 @@ inline void fused_init(FusedWork &w, cudaStream_t s) {
   if (w.enabled) cudaMemsetAsync(w.bar, 0, 64, s);
 }
 
-inline bool fused_supported(const FusedWork &w, int B = 1) {
-  return w.enabled && B >= 1 && B <= kFusedMaxB;
+// neurons per stage (NA template bound and runtime G) and P1 rows per stage
+inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *NA, int *G, int *RP1) {
+  const size_t nb = (size_t)d * 2 * (reglu ? 3 : 2);
+  const int g = (int)(w.stage_bytes / nb);
+  *NA = g >= 2 ? 8 : 1;
+  *G = std::min(*NA, std::max(1, g));
+  const int rp = (int)(w.stage_bytes / ((size_t)d * 2));
+  *RP1 = std::max(1, std::min(*NA == 1 ? 2 : 8, rp));
 }
 
-template <typename T, int B, bool REGLU, int CP, int G, int RP1>
+inline bool fused_supported(const FusedWork &w, int B = 1) {
+  if (!w.enabled || B < 1 || B > kFusedMaxB) return false;
+  const int ch = fused_ch(w.d);
+  if (ch * 8 * B > 64) return false;  // register-resident x / y per group thread
+  int NA, G, RP1;
+  fused_geometry(w, w.d, w.reglu, &NA, &G, &RP1);
+  // the instantiated (CH, NA) combinations (fused_launch)
+  if (ch <= 2) return true;
+  return NA == 1 && (ch == 3 || ch == 4 || (B == 1 && (ch == 6 || ch == 8)));
+}
+
+template <typename T, int B, bool REGLU, int CH, int NA>
 inline cudaError_t fused_launch_t(FusedWork &w, const FusedParams &prm, cudaStream_t s) {
-  auto kern = k_layer<T, B, REGLU, CP, G, RP1>;
+  auto kern = k_layer<T, B, REGLU, CH, NA>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, w.smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -776,15 +843,6 @@ inline cudaError_t fused_launch_t(FusedWork &w, const FusedParams &prm, cudaStre
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, prm);
-}
-
-// neurons per stage and P1 rows per stage, from the stage size (same rule on both sides)
-inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *G, int *RP1, int *CP) {
-  const size_t nb = (size_t)d * 2 * (reglu ? 3 : 2);
-  const int g = (int)(w.stage_bytes / nb);
-  *G = g >= 8 ? 8 : (g >= 2 ? 2 : 1);
-  *CP = (d / 8 + kConsumers - 1) / kConsumers;
-  *RP1 = (*G == 8) ? 8 : (*CP == 1 ? 4 : 2);
 }
 
 template <typename T>
@@ -818,23 +876,23 @@ inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*
   p.bar = w.bar;
   p.NS = w.NS;
   p.stage_bytes = w.stage_bytes;
-  p.rows_p1 = w.rows_p1;
   p.words_p2 = w.words_p2;
   p.idcap = w.idcap;
   p.wcap = w.wcap;
   p.trace = w.trace;
-  int G, RP1, CP;
-  fused_geometry(w, a.d, a.reglu, &G, &RP1, &CP);
+  int NA, G, RP1;
+  fused_geometry(w, a.d, a.reglu, &NA, &G, &RP1);
   p.G = G;
   p.rows_p1 = RP1;
-#define PI_FL(NB, RG, CPV, GV, RV)                                                         \
-  if (a.B == NB && a.reglu == RG && CP == CPV && G == GV && RP1 == RV)                     \
-    return fused_launch_t<T, NB, RG, CPV, GV, RV>(w, p, s);
-#define PI_FL_B(NB, RG)                                                                    \
-  PI_FL(NB, RG, 1, 8, 8) PI_FL(NB, RG, 1, 2, 4) PI_FL(NB, RG, 1, 1, 4) PI_FL(NB, RG, 2, 1, 2) \
-  PI_FL(NB, RG, 3, 1, 2)
-  PI_FL_B(1, false) PI_FL_B(1, true) PI_FL_B(2, false) PI_FL_B(2, true)
-#undef PI_FL_B
+  const int CH = fused_ch(a.d);
+#define PI_FL(NB, RG, CHV, NAV) \
+  if (a.B == NB && a.reglu == RG && CH == CHV && NA == NAV) return fused_launch_t<T, NB, RG, CHV, NAV>(w, p, s);
+#define PI_FL_RG(NB, RG)                                                                       \
+  PI_FL(NB, RG, 1, 8) PI_FL(NB, RG, 1, 1) PI_FL(NB, RG, 2, 8) PI_FL(NB, RG, 2, 1) PI_FL(NB, RG, 3, 1) \
+  PI_FL(NB, RG, 4, 1)
+  PI_FL_RG(1, false) PI_FL_RG(1, true) PI_FL_RG(2, false) PI_FL_RG(2, true)
+  PI_FL(1, false, 6, 1) PI_FL(1, true, 6, 1) PI_FL(1, false, 8, 1) PI_FL(1, true, 8, 1)
+#undef PI_FL_RG
 #undef PI_FL
   return cudaErrorNotSupported;
 }
