@@ -234,7 +234,6 @@ __device__ __forceinline__ float up_total(const float *red, int i) {
 template <typename T, int B, bool REGLU, int CH, int NA>
 __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p) {
   constexpr int RPM = (NA == 1) ? 2 : 8;      // max P1 rows per stage
-  constexpr int RW = (B == 1) ? 16 : 8;       // P2 rows per transpose reduction
   extern __shared__ __align__(128) uint8_t fsmem[];
   uint8_t *smem = fsmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -250,7 +249,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint64_t *ids_ready = hready + NS;
   float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][8][32]
   float *hs = red + 2 * kGroupWarps * kRedStride;                    // [NS][NA*B]
-  float *s_b2 = hs + NS * NA * B;                                    // [wcap*32]
+  float *zbuf = hs + NS * NA * B;                                    // [2][B][kMaxWordsP2*32]
+  float *s_b2 = zbuf + 2 * B * kMaxWordsP2 * 32;                     // [wcap*32]
   float *s_bup = s_b2 + p.wcap * 32;                                 // [idcap]
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
@@ -434,7 +434,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   if (trace && tid == 0) trace[2] = globaltimer();
 
   // ---------------- phase 2 (down group): z = P2 g + b2, bits, union, counts ----------------
+  // All 8 down warps share each stage: warp w takes rows {4 (w + 8 k) .. +3}; each lane owns
+  // 16-byte chunks of r, a 4-row transpose reduction leaves row (lane & 3)'s logit in lanes
+  // 0..3, logits go to zbuf, and after a group barrier one warp per mask word ballots.
   if (!is_up) {
+    constexpr int R4 = 4;
     const int rchunks = r >> 3;
     float gr[kMaxCG][8][B];
 #pragma unroll
@@ -454,54 +458,48 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
     }
     int my_count = 0;
-    for (int st = gw; st < st_p2; st += kGroupWarps) {
+    for (int st = 0; st < st_p2; ++st) {
       const uint32_t it = st_p1 + st;
       const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
       const int nrows = min(m, wb * 32) - wa * 32;
+      float *zb = zbuf + (st & 1) * (B * kMaxWordsP2 * 32);   // double-buffered by stage parity
       wait_full(it);
       const uint8_t *buf = stage_ptr(it);
-      for (int wl = 0; wl < wb - wa; ++wl) {
-        float zfin[B];
+      for (int rb0 = gw * R4; rb0 < nrows; rb0 += kGroupWarps * R4) {
+        float v[B * R4];
 #pragma unroll
-        for (int b = 0; b < B; ++b) zfin[b] = 0.f;
+        for (int i = 0; i < B * R4; ++i) v[i] = 0.f;
 #pragma unroll
-        for (int q = 0; q < 32 / RW; ++q) {
-          float v[B][RW];
+        for (int i = 0; i < R4; ++i) {
+          const int row = rb0 + i;
+          if (row < nrows) {
+            const uint8_t *rowp = buf + (size_t)row * r * 2;
 #pragma unroll
-          for (int b = 0; b < B; ++b)
+            for (int cq = 0; cq < kMaxCG; ++cq) {
+              const int ch = lane + cq * 32;
+              if (ch < rchunks) {
+                float wf[8];
+                WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wf);
 #pragma unroll
-            for (int i = 0; i < RW; ++i) v[b][i] = 0.f;
+                for (int b = 0; b < B; ++b)
 #pragma unroll
-          for (int i = 0; i < RW; ++i) {
-            const int row = wl * 32 + q * RW + i;
-            if (row < nrows) {
-              const uint8_t *rowp = buf + (size_t)row * r * 2;
-#pragma unroll
-              for (int cq = 0; cq < kMaxCG; ++cq) {
-                const int ch = lane + cq * 32;
-                if (ch < rchunks) {
-                  float wf[8];
-                  WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wf);
-#pragma unroll
-                  for (int b = 0; b < B; ++b)
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) v[b][i] = fmaf(wf[e], gr[cq][e][b], v[b][i]);
-                }
+                  for (int e = 0; e < 8; ++e) v[b * R4 + i] = fmaf(wf[e], gr[cq][e][b], v[b * R4 + i]);
               }
             }
           }
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            const float z = warp_reduce_multi<RW>(v[b]);
-            if (lane / RW == q) zfin[b] = z;      // lane l ends up holding row l of the word
-          }
         }
-        const int rl = wl * 32 + lane;            // row of this lane, stage-local
+        const float z = warp_reduce_multi<B * R4>(v);   // lane l: token (l / R4) % B, row l % R4
+        if (lane < B * R4) zb[(lane / R4) * (kMaxWordsP2 * 32) + rb0 + (lane % R4)] = z;
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(kGroup) : "memory");   // down group: stage read, zbuf full
+      if (gt == 0) mbar_arrive_cnt(&empty[it % NS], kGroupWarps);
+      for (int wl = gw; wl < wb - wa; wl += kGroupWarps) {
+        const int rl = wl * 32 + lane;
         const int zoff = (wa - w0) * 32;
         uint32_t u = 0;
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-          const float z = (rl < nrows) ? zfin[b] + s_b2[zoff + rl] : __int_as_float(0x7fc00000);
+          const float z = (rl < nrows) ? zb[b * (kMaxWordsP2 * 32) + rl] + s_b2[zoff + rl] : __int_as_float(0x7fc00000);
           const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
           u |= bits;
           if (lane == 0) p.mask[(size_t)b * p.words + wa + wl] = bits;
@@ -511,8 +509,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           my_count += __popc(u);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[it % NS], kGroupWarps);
     }
     if (lane == 0 && my_count) atomicAdd(&s_count, my_count);
   }
@@ -789,7 +785,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const int words_all = (m + 31) / 32;
   w.wcap = (words_all + w.P - 1) / w.P + 1;
   const size_t extra = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 256;
+                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)2 * kFusedMaxB * kMaxWordsP2 * 32 * 4 +
+                       (size_t)w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 256;
   w.smem = (int)((size_t)w.NS * sb + extra);
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, 64)) return false;
