@@ -187,10 +187,10 @@ pi_status pi_stack_forward_host(pi_layer *const *layers, int32_t n_layers, const
 
 /* Profiling aid (tracing): when dev_buf is non-NULL, every later pi_layer_forward that runs
  * the fused kernel has each CTA's thread 0 write globaltimer (ns) stamps of its phase
- * boundaries to dev_buf[cta * 128 + k]: 0 start, 1 P1 done, 2 after grid barrier 1, 3 P2 done,
+ * boundaries to dev_buf[cta * 256 + k]: 0 start, 1 P1 done, 2 after grid barrier 1, 3 P2 done,
  * 4 after grid barrier 2, 5 ids extracted, 6 FFN done, 7 after grid barrier 3, 8 end;
  * [16 + i] when ring stage i became readable, [72 + i] when the producer issued it (i < 56).
- * dev_buf: dev uint64 [num_sms * 128]; NULL turns tracing off.  Errors: INVALID_ARGUMENT. */
+ * [128..191] phase-2 stage detail.  dev_buf: dev uint64 [num_sms * 256]; NULL turns tracing off.  Errors: INVALID_ARGUMENT. */
 pi_status pi_layer_set_trace(pi_layer *L, uint64_t *dev_buf);
 
 /* Neuron -> shard placement (host, deterministic).  Adapts the paper's ILP

@@ -139,13 +139,26 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// 128-bit shared-memory load (LDS.128) from a ring stage; volatile keeps it after the mbarrier wait
+// 128-bit shared-memory load (LDS.128) from a ring stage.  A plain (non-volatile) load, so the
+// compiler can batch the loads of several rows; the mbarrier wait before it carries a "memory"
+// clobber, which keeps every such load after the wait.
 __device__ __forceinline__ Pack8 lds128(const void *p) {
+  const uint4 v = *reinterpret_cast<const uint4 *>(p);
   Pack8 r;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.u[0]), "=r"(r.u[1]), "=r"(r.u[2]), "=r"(r.u[3])
-               : "r"(smem_addr(p)));
+  r.u[0] = v.x;
+  r.u[1] = v.y;
+  r.u[2] = v.z;
+  r.u[3] = v.w;
   return r;
+}
+// Branch-free guarded load: reads base + off if ok, else base (always valid), and returns zeros
+// when !ok.  Keeps the per-stage loops free of branches so the loads of a whole stage issue
+// back to back.
+__device__ __forceinline__ Pack8 lds128z(const uint8_t *base, size_t off, bool ok) {
+  Pack8 w = lds128(base + (ok ? off : 0));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w.u[k] = ok ? w.u[k] : 0u;
+  return w;
 }
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
@@ -227,6 +240,106 @@ __device__ __forceinline__ float up_total(const float *red, int i) {
 }
 
 // ---------------------------------------------------------------------------
+// phase 2: z = P2 g + b2 ; bit = z > t ; ballot.  All 16 consumer warps share each ring stage
+// (a block of mask words): warp w takes rows {R (w + 16 k) .. +R-1} (R = 2 / B), each lane owns
+// CG 16-byte chunks of r (g for those chunks in registers), a transpose reduction leaves each
+// (token, row) logit in one lane, logits go to zbuf, and after a consumer barrier one warp per
+// mask word ballots, writes the per-token words, the union word and its popcount.
+// ---------------------------------------------------------------------------
+struct P2Ctx {
+  uint8_t *stages;
+  uint64_t *full, *empty;
+  float *zbuf, *s_b2;
+  int *s_count;
+  unsigned long long *trace;
+  int NS, SB, st_p1, st_p2, w0, w1, m, r, words, words_p2;
+  float t;
+  const float *g;
+  uint32_t *mask, *uni;
+};
+
+template <typename T, int B, int CG>
+__device__ __forceinline__ void p2_phase(const P2Ctx &x) {
+  constexpr int RR = (B == 1) ? 2 : 1;   // rows per warp per iteration
+  constexpr int NV = Pow2Ceil<RR * B>::v;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rchunks = x.r >> 3;
+  float gr[CG][8][B];
+#pragma unroll
+  for (int q = 0; q < CG; ++q) {
+    const int ch = lane + q * 32;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (ch < rchunks) {
+        const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(x.g + (size_t)b * x.r + ch * 8));
+        const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(x.g + (size_t)b * x.r + ch * 8) + 1);
+        gr[q][0][b] = a0.x; gr[q][1][b] = a0.y; gr[q][2][b] = a0.z; gr[q][3][b] = a0.w;
+        gr[q][4][b] = a1.x; gr[q][5][b] = a1.y; gr[q][6][b] = a1.z; gr[q][7][b] = a1.w;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) gr[q][e][b] = 0.f;
+      }
+    }
+  }
+  int my_count = 0;
+  for (int st = 0; st < x.st_p2; ++st) {
+    const uint32_t it = x.st_p1 + st;
+    const int wa = x.w0 + st * x.words_p2, wb = min(x.w1, wa + x.words_p2);
+    const int nrows = min(x.m, wb * 32) - wa * 32;
+    float *zb = x.zbuf + (st & 1) * (B * kMaxWordsP2 * 32);   // double-buffered by stage parity
+    mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
+    if (x.trace && tid == 0 && it < 56) x.trace[16 + it] = globaltimer();
+    const uint8_t *buf = x.stages + (size_t)(it % x.NS) * x.SB;
+    for (int rb0 = warp * RR; rb0 < nrows; rb0 += kConsumerWarps * RR) {
+      float v[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[i] = 0.f;
+      Pack8 wv[RR][CG];
+#pragma unroll
+      for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int q = 0; q < CG; ++q) {
+          const int ch = lane + q * 32;
+          wv[i][q] = lds128z(buf, (size_t)(rb0 + i) * x.r * 2 + (size_t)ch * 16, rb0 + i < nrows && ch < rchunks);
+        }
+#pragma unroll
+      for (int i = 0; i < RR; ++i)
+#pragma unroll
+        for (int q = 0; q < CG; ++q) {
+          float wf[8];
+          WT<T>::unpack(wv[i][q], wf);
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[b * RR + i] = fmaf(wf[e], gr[q][e][b], v[b * RR + i]);
+        }
+      const float z = warp_reduce_multi<NV>(v);   // lane l: token (l / RR) % B, row l % RR
+      if (lane < RR * B) zb[(lane / RR) * (kMaxWordsP2 * 32) + rb0 + (lane % RR)] = z;
+    }
+    consumers_sync();   // stage fully read, zbuf complete
+    if (tid == 0) mbar_arrive_cnt(&x.empty[it % x.NS], kGroupWarps);
+    for (int wl = warp; wl < wb - wa; wl += kConsumerWarps) {
+      const int rl = wl * 32 + lane;
+      const int zoff = (wa - x.w0) * 32;
+      uint32_t u = 0;
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const float z = (rl < nrows) ? zb[b * (kMaxWordsP2 * 32) + rl] + x.s_b2[zoff + rl] : __int_as_float(0x7fc00000);
+        const uint32_t bits = __ballot_sync(0xffffffffu, z > x.t);
+        u |= bits;
+        if (lane == 0) x.mask[(size_t)b * x.words + wa + wl] = bits;
+      }
+      if (lane == 0) {
+        x.uni[wa + wl] = u;
+        my_count += __popc(u);
+      }
+    }
+  }
+  if (lane == 0 && my_count) atomicAdd(x.s_count, my_count);
+  if (x.trace && tid == 0) x.trace[3] = globaltimer();
+}
+
+// ---------------------------------------------------------------------------
 // the kernel
 //   CH : 16-byte chunks of d per group thread (chunk = t + 256 q, q < CH)
 //   NA : max neurons per ring stage (also bounds P1 rows per stage: NA == 1 -> 2, else 8)
@@ -258,7 +371,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
-  unsigned long long *trace = p.trace ? p.trace + (size_t)c * 128 : nullptr;
+  unsigned long long *trace = p.trace ? p.trace + (size_t)c * 256 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
 
   // ---- work split (identical on producer and consumer side) ----
@@ -341,7 +454,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   auto stage_ptr = [&](uint32_t it) { return stages + (size_t)(it % NS) * SB; };
   auto wait_full = [&](uint32_t it) {
     mbar_wait(&full[it % NS], (it / NS) & 1);
-    if (trace && tid == 0 && it < 56) trace[16 + it] = globaltimer();
+    if (trace && (tid == 0 || (tid == kGroup && it >= (uint32_t)st_p1 && it < (uint32_t)(st_p1 + st_p2))) && it < 56)
+      trace[16 + it] = globaltimer();
   };
 
   float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
@@ -402,19 +516,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       for (int i = 0; i < RPM * B; ++i) acc[i] = 0.f;
 #pragma unroll
       for (int k = 0; k < RPM; ++k) {
-        if (k < kn) {
 #pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int ch = gt + q * kGroup;
-            if (ch < chunks) {
-              float wf[8];
-              WT<T>::unpack(lds128(buf + (size_t)k * row_dn + (size_t)ch * 16), wf);
+        for (int q = 0; q < CH; ++q) {
+          const int ch = gt + q * kGroup;
+          float wf[8];
+          WT<T>::unpack(lds128z(buf, (size_t)k * row_dn + (size_t)ch * 16, k < kn && ch < chunks), wf);
 #pragma unroll
-              for (int b = 0; b < B; ++b)
+          for (int b = 0; b < B; ++b)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
-            }
-          }
+            for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
         }
       }
       float *rb = red + (it & 1) * kGroupWarps * kRedStride;
@@ -433,86 +543,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   grid_sync(p.bar, P);
   if (trace && tid == 0) trace[2] = globaltimer();
 
-  // ---------------- phase 2 (down group): z = P2 g + b2, bits, union, counts ----------------
-  // All 8 down warps share each stage: warp w takes rows {4 (w + 8 k) .. +3}; each lane owns
-  // 16-byte chunks of r, a 4-row transpose reduction leaves row (lane & 3)'s logit in lanes
-  // 0..3, logits go to zbuf, and after a group barrier one warp per mask word ballots.
-  if (!is_up) {
-    constexpr int R4 = 4;
-    const int rchunks = r >> 3;
-    float gr[kMaxCG][8][B];
-#pragma unroll
-    for (int q = 0; q < kMaxCG; ++q) {
-      const int ch = lane + q * 32;
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        if (ch < rchunks) {
-          const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(p.g + (size_t)b * r + ch * 8));
-          const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(p.g + (size_t)b * r + ch * 8) + 1);
-          gr[q][0][b] = a0.x; gr[q][1][b] = a0.y; gr[q][2][b] = a0.z; gr[q][3][b] = a0.w;
-          gr[q][4][b] = a1.x; gr[q][5][b] = a1.y; gr[q][6][b] = a1.z; gr[q][7][b] = a1.w;
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) gr[q][e][b] = 0.f;
-        }
-      }
-    }
-    int my_count = 0;
-    for (int st = 0; st < st_p2; ++st) {
-      const uint32_t it = st_p1 + st;
-      const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
-      const int nrows = min(m, wb * 32) - wa * 32;
-      float *zb = zbuf + (st & 1) * (B * kMaxWordsP2 * 32);   // double-buffered by stage parity
-      wait_full(it);
-      const uint8_t *buf = stage_ptr(it);
-      for (int rb0 = gw * R4; rb0 < nrows; rb0 += kGroupWarps * R4) {
-        float v[B * R4];
-#pragma unroll
-        for (int i = 0; i < B * R4; ++i) v[i] = 0.f;
-#pragma unroll
-        for (int i = 0; i < R4; ++i) {
-          const int row = rb0 + i;
-          if (row < nrows) {
-            const uint8_t *rowp = buf + (size_t)row * r * 2;
-#pragma unroll
-            for (int cq = 0; cq < kMaxCG; ++cq) {
-              const int ch = lane + cq * 32;
-              if (ch < rchunks) {
-                float wf[8];
-                WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wf);
-#pragma unroll
-                for (int b = 0; b < B; ++b)
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) v[b * R4 + i] = fmaf(wf[e], gr[cq][e][b], v[b * R4 + i]);
-              }
-            }
-          }
-        }
-        const float z = warp_reduce_multi<B * R4>(v);   // lane l: token (l / R4) % B, row l % R4
-        if (lane < B * R4) zb[(lane / R4) * (kMaxWordsP2 * 32) + rb0 + (lane % R4)] = z;
-      }
-      asm volatile("bar.sync 3, %0;" ::"n"(kGroup) : "memory");   // down group: stage read, zbuf full
-      if (gt == 0) mbar_arrive_cnt(&empty[it % NS], kGroupWarps);
-      for (int wl = gw; wl < wb - wa; wl += kGroupWarps) {
-        const int rl = wl * 32 + lane;
-        const int zoff = (wa - w0) * 32;
-        uint32_t u = 0;
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          const float z = (rl < nrows) ? zb[b * (kMaxWordsP2 * 32) + rl] + s_b2[zoff + rl] : __int_as_float(0x7fc00000);
-          const uint32_t bits = __ballot_sync(0xffffffffu, z > p.t);
-          u |= bits;
-          if (lane == 0) p.mask[(size_t)b * p.words + wa + wl] = bits;
-        }
-        if (lane == 0) {
-          p.uni[wa + wl] = u;
-          my_count += __popc(u);
-        }
-      }
-    }
-    if (lane == 0 && my_count) atomicAdd(&s_count, my_count);
+  // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
+  {
+    P2Ctx ctx{stages, full, empty, zbuf, s_b2, &s_count, trace, NS, SB, st_p1, st_p2, w0, w1, m, r, p.words,
+              p.words_p2, p.t, p.g, p.mask, p.uni};
+    const int cg = ((r >> 3) + 31) / 32;
+    if (cg <= 1) p2_phase<T, B, 1>(ctx);
+    else if (cg == 2) p2_phase<T, B, 2>(ctx);
+    else if (cg == 3) p2_phase<T, B, 3>(ctx);
+    else p2_phase<T, B, 4>(ctx);
   }
-  if (trace && tid == 0) trace[3] = globaltimer();
   consumers_sync();
   if (tid == 0) p.counts[c] = s_count;
   grid_sync(p.bar, P);
@@ -621,34 +661,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       for (int i = 0; i < NV; ++i) acc[i] = 0.f;
 #pragma unroll
       for (int g = 0; g < NA; ++g) {
-        if (g < kn) {
-          const uint8_t *rowp = buf + (size_t)g * nb;
+        const size_t go = (size_t)g * nb;
 #pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int ch = gt + q * kGroup;
-            if (ch < chunks) {
-              float wu[8];
-              if (REGLU) {
-                float wg[8];
-                WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wg);
-                WT<T>::unpack(lds128(rowp + (size_t)d * 2 + (size_t)ch * 16), wu);
+        for (int q = 0; q < CH; ++q) {
+          const int ch = gt + q * kGroup;
+          const bool ok = g < kn && ch < chunks;
+          float wu[8];
+          if (REGLU) {
+            float wg[8];
+            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
+            WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
 #pragma unroll
-                for (int b = 0; b < B; ++b)
+            for (int b = 0; b < B; ++b)
 #pragma unroll
-                  for (int e = 0; e < 8; ++e)
-                    acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
-              } else {
-                WT<T>::unpack(lds128(rowp + (size_t)ch * 16), wu);
-              }
-#pragma unroll
-              for (int b = 0; b < B; ++b)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-                  acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
-                }
-            }
+              for (int e = 0; e < 8; ++e)
+                acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+          } else {
+            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
           }
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+              acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+            }
         }
       }
       float *rb = red + (f & 1) * kGroupWarps * kRedStride;
@@ -682,23 +719,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       const float *hh = hs + (it % NS) * (NA * B);
 #pragma unroll
       for (int g = 0; g < NA; ++g) {
-        if (g < kn) {
-          float h[B];
+        float h[B];
 #pragma unroll
-          for (int b = 0; b < B; ++b) h[b] = hh[g * B + b];
-          const uint8_t *dn = buf + (size_t)g * nb + row_up;
+        for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
+        const size_t go = (size_t)g * nb + row_up;
 #pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int ch = gt + q * kGroup;
-            if (ch < chunks) {
-              float wf[8];
-              WT<T>::unpack(lds128(dn + (size_t)ch * 16), wf);
+        for (int q = 0; q < CH; ++q) {
+          const int ch = gt + q * kGroup;
+          float wf[8];
+          WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
 #pragma unroll
-              for (int b = 0; b < B; ++b)
+          for (int b = 0; b < B; ++b)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
-            }
-          }
+            for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
         }
       }
       __syncwarp();

@@ -29,7 +29,7 @@ def main():
     cfg = gen.CONFIGS[a.config]
     st, _ = build_stack(cfg, n_layers=min(a.layers, cfg.layers), device="cuda", max_batch=a.batch)
     P = st.layers[0].info.num_sms
-    buf = torch.zeros(P * 128, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(P * 256, dtype=torch.int64, device="cuda")
     x = gen.tokens(a.batch, cfg.d, seed=3, device="cuda")
     y = torch.empty_like(x)
     n = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -42,7 +42,7 @@ def main():
         L.forward(x, y, None, None, n)
         torch.cuda.synchronize()
         L.set_trace(None)
-        full = buf.view(P, 128).cpu().numpy().astype(np.float64)
+        full = buf.view(P, 256).cpu().numpy().astype(np.float64)
         t = full[:, :9]
         t0 = t[:, 0].min()
         rel = (t - t0) / 1e3
@@ -50,6 +50,7 @@ def main():
         ready = np.where(full[:, 16:72] > 0, (full[:, 16:72] - t0) / 1e3, np.nan)
         issue = np.where(full[:, 72:128] > 0, (full[:, 72:128] - t0) / 1e3, np.nan)
         stage_rows.append((ready, issue))
+        dbg = np.where(full[:, 128:192] > 0, (full[:, 128:192] - t0) / 1e3, np.nan)
         x = y.clone()
     R = np.stack(rows[2:])                    # drop warm-up reps
     mean = R.mean(axis=(0, 1))
@@ -59,6 +60,7 @@ def main():
            "phases_us_mean_over_ctas": dict(zip(NAMES, np.round(mean, 2).tolist())),
            "phases_us_max_over_ctas": dict(zip(NAMES, np.round(mx, 2).tolist())),
            "ideal_us_at_peak": round(nb / 6560.6e9 * 1e6, 2)}
+    out["cta0_p2_detail_us"] = np.round(dbg[0].reshape(16, 4)[:, :3], 2).tolist()
     rd, iss = stage_rows[-1]
     for cta in (0, P // 2):
         k = int(np.sum(~np.isnan(rd[cta])))
