@@ -287,6 +287,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     const int wa = x.w0 + st * x.words_p2, wb = min(x.w1, wa + x.words_p2);
     const int nrows = min(x.m, wb * 32) - wa * 32;
     float *zb = x.zbuf + (st & 1) * (B * kMaxWordsP2 * 32);   // double-buffered by stage parity
+    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 3] = clock64();
     mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
     if (x.trace && tid == 0 && it < 56) x.trace[16 + it] = globaltimer();
     const uint8_t *buf = x.stages + (size_t)(it % x.NS) * x.SB;
@@ -316,7 +317,9 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       const float z = warp_reduce_multi<NV>(v);   // lane l: token (l / RR) % B, row l % RR
       if (lane < RR * B) zb[(lane / RR) * (kMaxWordsP2 * 32) + rb0 + (lane % RR)] = z;
     }
+    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 0] = clock64();
     consumers_sync();   // stage fully read, zbuf complete
+    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 1] = clock64();
     if (tid == 0) mbar_arrive_cnt(&x.empty[it % x.NS], kGroupWarps);
     for (int wl = warp; wl < wb - wa; wl += kConsumerWarps) {
       const int rl = wl * 32 + lane;
@@ -334,6 +337,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
         my_count += __popc(u);
       }
     }
+    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 2] = clock64();
   }
   if (lane == 0 && my_count) atomicAdd(x.s_count, my_count);
   if (x.trace && tid == 0) x.trace[3] = globaltimer();

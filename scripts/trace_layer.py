@@ -50,7 +50,9 @@ def main():
         ready = np.where(full[:, 16:72] > 0, (full[:, 16:72] - t0) / 1e3, np.nan)
         issue = np.where(full[:, 72:128] > 0, (full[:, 72:128] - t0) / 1e3, np.nan)
         stage_rows.append((ready, issue))
-        dbg = np.where(full[:, 128:192] > 0, (full[:, 128:192] - t0) / 1e3, np.nan)
+        raw = full[:, 128:192].reshape(P, 16, 4)
+        base = raw[:, 0, 3:4]
+        dbg = np.where(raw > 0, raw - base[:, :, None] if False else raw - raw[:, :1, 3:4], np.nan)
         x = y.clone()
     R = np.stack(rows[2:])                    # drop warm-up reps
     mean = R.mean(axis=(0, 1))
@@ -60,7 +62,7 @@ def main():
            "phases_us_mean_over_ctas": dict(zip(NAMES, np.round(mean, 2).tolist())),
            "phases_us_max_over_ctas": dict(zip(NAMES, np.round(mx, 2).tolist())),
            "ideal_us_at_peak": round(nb / 6560.6e9 * 1e6, 2)}
-    out["cta0_p2_detail_us"] = np.round(dbg[0].reshape(16, 4)[:, :3], 2).tolist()
+    out["cta0_p2_detail_cycles(wait_start,computed,synced,balloted)"] = dbg[0][:, [3, 0, 1, 2]].astype(int).tolist() if not np.isnan(dbg[0][0, 0]) else []
     rd, iss = stage_rows[-1]
     for cta in (0, P // 2):
         k = int(np.sum(~np.isnan(rd[cta])))
