@@ -252,7 +252,7 @@ struct P2Ctx {
   float *zbuf, *s_b2;
   int *s_count;
   unsigned long long *trace;
-  int NS, SB, st_p1, st_p2, w0, w1, m, r, words, words_p2;
+  int NS, SB, st_p1, st_p2, w0, w1, m, r, words, words_p2, zst;
   float t;
   const float *g;
   uint32_t *mask, *uni;
@@ -281,13 +281,11 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       }
     }
   }
-  int my_count = 0;
   for (int st = 0; st < x.st_p2; ++st) {
     const uint32_t it = x.st_p1 + st;
     const int wa = x.w0 + st * x.words_p2, wb = min(x.w1, wa + x.words_p2);
     const int nrows = min(x.m, wb * 32) - wa * 32;
-    float *zb = x.zbuf + (st & 1) * (B * kMaxWordsP2 * 32);   // double-buffered by stage parity
-    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 3] = clock64();
+    const int zoff = (wa - x.w0) * 32;   // CTA-local row of this stage's first row
     mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
     if (x.trace && tid == 0 && it < 56) x.trace[16 + it] = globaltimer();
     const uint8_t *buf = x.stages + (size_t)(it % x.NS) * x.SB;
@@ -315,29 +313,29 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
             for (int e = 0; e < 8; ++e) v[b * RR + i] = fmaf(wf[e], gr[q][e][b], v[b * RR + i]);
         }
       const float z = warp_reduce_multi<NV>(v);   // lane l: token (l / RR) % B, row l % RR
-      if (lane < RR * B) zb[(lane / RR) * (kMaxWordsP2 * 32) + rb0 + (lane % RR)] = z;
+      if (lane < RR * B) x.zbuf[(lane / RR) * x.zst + zoff + rb0 + (lane % RR)] = z;
     }
-    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 0] = clock64();
-    consumers_sync();   // stage fully read, zbuf complete
-    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 1] = clock64();
-    if (tid == 0) mbar_arrive_cnt(&x.empty[it % x.NS], kGroupWarps);
-    for (int wl = warp; wl < wb - wa; wl += kConsumerWarps) {
-      const int rl = wl * 32 + lane;
-      const int zoff = (wa - x.w0) * 32;
-      uint32_t u = 0;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&x.empty[it % x.NS]);   // this warp is done with the stage
+  }
+  consumers_sync();   // every logit of this CTA's words is in zbuf
+  // ballots: one warp per mask word -> per-token words, union word, popcount
+  int my_count = 0;
+  for (int wl = warp; wl < x.w1 - x.w0; wl += kConsumerWarps) {
+    const int rl = wl * 32 + lane;
+    const bool valid = (x.w0 * 32 + rl) < x.m;
+    uint32_t u = 0;
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const float z = (rl < nrows) ? zb[b * (kMaxWordsP2 * 32) + rl] + x.s_b2[zoff + rl] : __int_as_float(0x7fc00000);
-        const uint32_t bits = __ballot_sync(0xffffffffu, z > x.t);
-        u |= bits;
-        if (lane == 0) x.mask[(size_t)b * x.words + wa + wl] = bits;
-      }
-      if (lane == 0) {
-        x.uni[wa + wl] = u;
-        my_count += __popc(u);
-      }
+    for (int b = 0; b < B; ++b) {
+      const float z = valid ? x.zbuf[b * x.zst + rl] + x.s_b2[rl] : __int_as_float(0x7fc00000);
+      const uint32_t bits = __ballot_sync(0xffffffffu, z > x.t);
+      u |= bits;
+      if (lane == 0) x.mask[(size_t)b * x.words + x.w0 + wl] = bits;
     }
-    if (x.trace && tid == 0 && st < 16) x.trace[128 + st * 4 + 2] = clock64();
+    if (lane == 0) {
+      x.uni[x.w0 + wl] = u;
+      my_count += __popc(u);
+    }
   }
   if (lane == 0 && my_count) atomicAdd(x.s_count, my_count);
   if (x.trace && tid == 0) x.trace[3] = globaltimer();
@@ -366,8 +364,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint64_t *ids_ready = hready + NS;
   float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][8][32]
   float *hs = red + 2 * kGroupWarps * kRedStride;                    // [NS][NA*B]
-  float *zbuf = hs + NS * NA * B;                                    // [2][B][kMaxWordsP2*32]
-  float *s_b2 = zbuf + 2 * B * kMaxWordsP2 * 32;                     // [wcap*32]
+  float *zbuf = hs + NS * NA * B;                                    // [B][wcap*32] logits of my words
+  float *s_b2 = zbuf + B * p.wcap * 32;                              // [wcap*32]
   float *s_bup = s_b2 + p.wcap * 32;                                 // [idcap]
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
@@ -391,7 +389,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kGroupWarps);
+      mbar_init(&empty[s], kConsumerWarps);
       mbar_init(&hready[s], 1);
     }
     mbar_init(ids_ready, 1);
@@ -533,7 +531,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
       float *rb = red + (it & 1) * kGroupWarps * kRedStride;
       up_partials<RPM * B>(acc, rb);
-      if (gt == 0) mbar_arrive_cnt(&empty[it % NS], kGroupWarps);  // every up warp has read the stage
+      if (gt == 0) mbar_arrive_cnt(&empty[it % NS], kConsumerWarps);  // every up warp has read the stage
       if (gt < kn * B) {
         const int k = gt / B, b = gt % B;
         const int j = c + (k0 + k) * P;
@@ -550,7 +548,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
   {
     P2Ctx ctx{stages, full, empty, zbuf, s_b2, &s_count, trace, NS, SB, st_p1, st_p2, w0, w1, m, r, p.words,
-              p.words_p2, p.t, p.g, p.mask, p.uni};
+              p.words_p2, p.wcap * 32, p.t, p.g, p.mask, p.uni};
     const int cg = ((r >> 3) + 31) / 32;
     if (cg <= 1) p2_phase<T, B, 1>(ctx);
     else if (cg == 2) p2_phase<T, B, 2>(ctx);
@@ -739,7 +737,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[it % NS]);
+      if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
     }
     // partial y of this CTA -> global
 #pragma unroll
@@ -822,8 +820,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const int words_all = (m + 31) / 32;
   w.wcap = (words_all + w.P - 1) / w.P + 1;
   const size_t extra = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)2 * kFusedMaxB * kMaxWordsP2 * 32 * 4 +
-                       (size_t)w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 256;
+                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 +
+                       (size_t)w.idcap * 9 + 256;
   w.smem = (int)((size_t)w.NS * sb + extra);
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, 64)) return false;

@@ -62,7 +62,6 @@ def main():
            "phases_us_mean_over_ctas": dict(zip(NAMES, np.round(mean, 2).tolist())),
            "phases_us_max_over_ctas": dict(zip(NAMES, np.round(mx, 2).tolist())),
            "ideal_us_at_peak": round(nb / 6560.6e9 * 1e6, 2)}
-    out["cta0_p2_detail_cycles(wait_start,computed,synced,balloted)"] = dbg[0][:, [3, 0, 1, 2]].astype(int).tolist() if not np.isnan(dbg[0][0, 0]) else []
     rd, iss = stage_rows[-1]
     for cta in (0, P // 2):
         k = int(np.sum(~np.isnan(rd[cta])))
