@@ -293,11 +293,22 @@ def main():
     realised = float(n_host.mean() / metas[0].m_local)
 
     # ---- dominant kernel: per-launch durations with CUDA events on the launching stream ----
+    # world 1: the stack kernel (one launch = one step through every layer);
+    # world > 1: the per-layer fused kernel (launches separated by the NCCL all-reduce)
     prof_steps = min(args.steps, 10)
     kt, kb = [], []
     for k in range(prof_steps):
         i = args.warmup + k
         st = stacks[i % copies]
+        if world == 1:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st.step(xs[i], y, None, bufs)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            kt.append(e0.elapsed_time(e1) / 1e3)
+            kb.append(float(bytes_step[k].sum()))
+            continue
         e0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
         e1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
         cur = xs[i]
@@ -306,8 +317,7 @@ def main():
             e0[l].record(stream)
             L.forward(cur, dst)
             e1[l].record(stream)
-            if world > 1:
-                dist.all_reduce(dst)
+            dist.all_reduce(dst)
             cur = dst
         torch.cuda.synchronize()
         for l in range(n_layers):
@@ -318,7 +328,10 @@ def main():
     peak, peak_src = hbm_peak()
     achieved = bytes_launch / launch_s / 1e9
     launches_per_layer = int(stacks[0].layers[0].info.launches_per_forward)
-    roofline = {"bound": "hbm", "kernel": "pi_layer_forward (%d launch(es) per layer)" % launches_per_layer,
+    kname = ("k_layer x%d layers in one persistent launch (pi_stack_run)" % n_layers) if world == 1 and \
+        launches_per_layer == 1 else "pi_layer_forward (%d launch(es) per layer)" % launches_per_layer
+    launches_per_step = 1 if (world == 1 and launches_per_layer == 1) else n_layers * launches_per_layer
+    roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": None, "peak_source": peak_src,
                 "bytes_per_launch": int(bytes_launch), "launch_us": round(launch_s * 1e6, 2),
@@ -335,7 +348,7 @@ def main():
             i = args.warmup + k
             st = stacks[i % copies]
             if world == 1:
-                pi.pi_stack_forward_host(st.handles, xh[i], yh)
+                st.stack.run_host(xh[i], yh)
             else:
                 xd = xh[i].to(dev, non_blocking=True)
                 st.step(xd, y, None, bufs)
@@ -347,7 +360,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = {"value": B * args.steps / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": B * d * 4,
-               "d2h_bytes_per_step": B * d * 4, "api": "pi_stack_forward_host" if world == 1 else
+               "d2h_bytes_per_step": B * d * 4, "api": "pi_stack_run_host" if world == 1 else
                "host copy + pi_layer_forward + NCCL all_reduce per layer + host copy"}
 
     cpu = None
@@ -367,7 +380,7 @@ def main():
                "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
                               "p99": float(np.percentile(per_step, 99))},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": int(args.steps * n_layers * launches_per_layer), "clocks": clk}
+               "gpu_launches": int(args.steps * launches_per_step), "clocks": clk}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

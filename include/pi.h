@@ -185,6 +185,24 @@ pi_status pi_stack_forward(pi_layer *const *layers, int32_t n_layers, const floa
 pi_status pi_stack_forward_host(pi_layer *const *layers, int32_t n_layers, const float *x_host,
                                 int32_t B, float *y_host, pi_stream_t stream);
 
+/* A stack: L compatible layers (same d, m_local, rank, act, dtype, pred_act, flags,
+ * max_batch) run as ONE persistent kernel per decode step, x_{l+1} = y_l.  The kernel's TMA
+ * producer streams layer l+1's predictor rows while layer l finishes, and no launch gap
+ * separates the layers.  The stack keeps pointers to the layers (it does not own them);
+ * destroy the stack before its layers.  Errors: INVALID_ARGUMENT, SHAPE (incompatible
+ * layers), OUT_OF_MEMORY, CUDA. */
+typedef struct pi_stack pi_stack;
+pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, pi_stack **out);
+pi_status pi_stack_destroy(pi_stack *S);
+/* One decode step through the stack.  x, y: dev fp32 [B, d]; n_active_out: dev int32
+ * [n_layers] (each layer's union count) or NULL.  Falls back to one launch per layer when the
+ * fused kernel does not support the shape / batch.  Graph capturable. */
+pi_status pi_stack_run(pi_stack *S, const float *x, int32_t B, float *y, int32_t *n_active_out,
+                       pi_stream_t stream);
+/* pi_stack_run with HOST buffers (end-to-end path); returns after `stream` has finished. */
+pi_status pi_stack_run_host(pi_stack *S, const float *x_host, int32_t B, float *y_host,
+                            pi_stream_t stream);
+
 /* Profiling aid (tracing): when dev_buf is non-NULL, every later pi_layer_forward that runs
  * the fused kernel has each CTA's thread 0 write globaltimer (ns) stamps of its phase
  * boundaries to dev_buf[cta * 256 + k]: 0 start, 1 P1 done, 2 after grid barrier 1, 3 P2 done,

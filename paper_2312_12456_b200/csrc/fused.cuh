@@ -53,7 +53,7 @@ constexpr int kRedStride = 32;   // floats per warp in the up-group reduction bu
 
 struct FusedWork {
   bool enabled = false;
-  int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0;
+  int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0, part_off = 0;
   int d = 0, m = 0, r = 0;
   bool reglu = false;
   unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
@@ -62,6 +62,7 @@ struct FusedWork {
   int *counts = nullptr;              // [P]
   uint32_t *mask = nullptr;           // [maxB, words]
   uint32_t *uni = nullptr;            // [words]
+  float *xbuf = nullptr;              // [maxB, d] inter-layer activations (stack launch)
   unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
 };
 
@@ -76,21 +77,29 @@ struct FusedArgs {
   int32_t *ids_out, *n_out;
 };
 
-struct FusedParams {
+struct LayerW {  // one layer's library-owned weights (device pointers)
   const uint8_t *w_up, *w_down, *p_w1, *p_w2;
   const void *b_up, *b_down, *p_b1, *p_b2;
-  const float *x;
-  float *y;
-  int d, m, r, words, B;
   float t;
+  int pad;
+};
+
+struct FusedParams {
+  LayerW lw0;                 // the layer of a single-layer launch
+  const LayerW *lws;          // device array of L layers (stack launch) or NULL (use lw0)
+  int L;
+  const float *x;             // layer-0 input [B, d]
+  float *y;                   // last-layer output [B, d]
+  float *xbuf;                // inter-layer activations [B, d] (stack launch)
+  int d, m, r, words, B;
   int rmsnorm, pred_relu;
   uint32_t *mask, *uni;
-  int32_t *ids_out, *n_out;
+  int32_t *ids_out, *n_out;   // n_out: [L] union counts
   float *g, *ypart;
   int *counts;
   unsigned long long *bar;
-  int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap;
-  unsigned long long *trace;  // [P][128] timestamps (globaltimer ns) or NULL
+  int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off;
+  unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
 };
 
 // ---------------------------------------------------------------------------
@@ -248,7 +257,7 @@ __device__ __forceinline__ float up_total(const float *red, int i) {
 // ---------------------------------------------------------------------------
 struct P2Ctx {
   uint8_t *stages;
-  uint64_t *full, *empty;
+  uint64_t *full, *empty, *hready;
   float *zbuf, *s_b2;
   int *s_count;
   unsigned long long *trace;
@@ -315,6 +324,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       const float z = warp_reduce_multi<NV>(v);   // lane l: token (l / RR) % B, row l % RR
       if (lane < RR * B) x.zbuf[(lane / RR) * x.zst + zoff + rb0 + (lane % RR)] = z;
     }
+    if (tid == 0) mbar_arrive(&x.hready[it % x.NS]);   // keep hready phases = ring uses
     __syncwarp();
     if (lane == 0) mbar_arrive(&x.empty[it % x.NS]);   // this warp is done with the stage
   }
@@ -353,7 +363,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint8_t *smem = fsmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = gridDim.x, c = blockIdx.x;
-  const int d = p.d, r = p.r, m = p.m;
+  const int d = p.d, r = p.r, m = p.m, L = p.L;
   const int NS = p.NS, SB = p.stage_bytes, G = p.G, RP1 = p.rows_p1;
 
   // ---- shared memory carve-up ----
@@ -369,14 +379,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   float *s_bup = s_b2 + p.wcap * 32;                                 // [idcap]
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
-  __shared__ float s_scale[B];
+  float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // [8][pcap*B] phase-4 partials
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
   unsigned long long *trace = p.trace ? p.trace + (size_t)c * 256 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
 
-  // ---- work split (identical on producer and consumer side) ----
+  // ---- work split (identical on producer and consumer side, every layer) ----
   const int chunks = d >> 3;
   const int n_p1 = (r > c) ? (r - 1 - c) / P + 1 : 0;  // rows j = c + P*k
   const int st_p1 = (n_p1 + RP1 - 1) / RP1;
@@ -385,6 +395,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   const size_t row_up = (size_t)d * 2 * (REGLU ? 2 : 1);  // bytes of one up (gate|up) row
   const size_t row_dn = (size_t)d * 2;
   const size_t nb = row_up + row_dn;                       // bytes per neuron in a stage
+  auto layer = [&](int l) -> LayerW { return p.lws ? p.lws[l] : p.lw0; };
 
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -393,13 +404,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_init(&hready[s], 1);
     }
     mbar_init(ids_ready, 1);
-    s_count = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
   // =====================================================================================
-  // producer warp
+  // producer warp: streams layer after layer; runs ahead into the next layer's P1 and P2
+  // rows while the consumers finish the current layer (bounded by the ring)
   // =====================================================================================
   if (warp == kConsumerWarps) {
     if (lane != 0) return;
@@ -413,33 +424,36 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
     };
-    for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
-      const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
-      uint8_t *dst = acquire((uint32_t)(kn * row_dn));
-      const int s = it % NS;
-      for (int k = 0; k < kn; ++k) {
-        const int j = c + (k0 + k) * P;
-        bulk_g2s(dst + (size_t)k * row_dn, p.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
+    for (int l = 0; l < L; ++l) {
+      const LayerW lw = layer(l);
+      for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
+        const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
+        uint8_t *dst = acquire((uint32_t)(kn * row_dn));
+        const int s = it % NS;
+        for (int k = 0; k < kn; ++k) {
+          const int j = c + (k0 + k) * P;
+          bulk_g2s(dst + (size_t)k * row_dn, lw.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
+        }
       }
-    }
-    const size_t rowb2 = (size_t)r * 2;
-    for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 rows of words [w0, w1), contiguous
-      const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
-      const int ra = wa * 32, rb = min(m, wb * 32);
-      const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
-      uint8_t *dst = acquire(bytes);
-      bulk_g2s(dst, p.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
-    }
-    mbar_wait(ids_ready, 0);                     // phase 3: after the ids are published
-    const int n_mine = s_k1 - s_k0;
-    for (int k0 = 0; k0 < n_mine; k0 += G, ++it) {
-      const int kn = min(G, n_mine - k0);
-      uint8_t *dst = acquire((uint32_t)(kn * nb));
-      const int s = it % NS;
-      for (int k = 0; k < kn; ++k) {
-        const int i = s_ids[k0 + k];
-        bulk_g2s(dst + (size_t)k * nb, p.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
-        bulk_g2s(dst + (size_t)k * nb + row_up, p.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+      const size_t rowb2 = (size_t)r * 2;
+      for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 rows of words [w0, w1), contiguous
+        const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
+        const int ra = wa * 32, rb = min(m, wb * 32);
+        const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
+        uint8_t *dst = acquire(bytes);
+        bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
+      }
+      mbar_wait(ids_ready, l & 1);                 // phase 3: after the ids are published
+      const int n_mine = s_k1 - s_k0;
+      for (int k0 = 0; k0 < n_mine; k0 += G, ++it) {
+        const int kn = min(G, n_mine - k0);
+        uint8_t *dst = acquire((uint32_t)(kn * nb));
+        const int s = it % NS;
+        for (int k = 0; k < kn; ++k) {
+          const int i = s_ids[k0 + k];
+          bulk_g2s(dst + (size_t)k * nb, lw.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
+          bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+        }
       }
     }
     // drain: do not retire before the consumers released every stage
@@ -454,341 +468,354 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   const int gt = is_up ? tid : tid - kGroup;   // thread index inside its group
   const int gw = gt >> 5;                      // warp index inside its group
   auto stage_ptr = [&](uint32_t it) { return stages + (size_t)(it % NS) * SB; };
-  auto wait_full = [&](uint32_t it) {
-    mbar_wait(&full[it % NS], (it / NS) & 1);
-    if (trace && (tid == 0 || (tid == kGroup && it >= (uint32_t)st_p1 && it < (uint32_t)(st_p1 + st_p2))) && it < 56)
-      trace[16 + it] = globaltimer();
-  };
+  uint32_t ring = 0;                           // ring position of this layer's first stage
 
-  float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
-  float sc[B];
-  if (is_up) {
+  for (int l = 0; l < L; ++l) {
+    const LayerW lw = layer(l);
+    const float *xin = (l == 0) ? p.x : p.xbuf;
+    float *yout = (l == L - 1) ? p.y : p.xbuf;
+    unsigned long long *tr = (l == 0) ? trace : nullptr;
+    auto wait_full = [&](uint32_t it) {
+      mbar_wait(&full[it % NS], (it / NS) & 1);
+      if (tr && tid == 0 && it < 56) tr[16 + it] = globaltimer();
+    };
+    if (tid == 0) s_count = 0;
+
+    float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
+    float sc[B];
+    if (is_up) {
 #pragma unroll
-    for (int q = 0; q < CH; ++q) {
-      const int ch = gt + q * kGroup;
+      for (int q = 0; q < CH; ++q) {
+        const int ch = gt + q * kGroup;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          if (ch < chunks) {
+            const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8));
+            const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8) + 1);
+            xr[q][0][b] = a0.x; xr[q][1][b] = a0.y; xr[q][2][b] = a0.z; xr[q][3][b] = a0.w;
+            xr[q][4][b] = a1.x; xr[q][5][b] = a1.y; xr[q][6][b] = a1.z; xr[q][7][b] = a1.w;
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
+          }
+        }
+      }
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        if (ch < chunks) {
-          float v[8];
-          ld_x8(p.x + (size_t)b * d + ch * 8, v);
+        float ss = 0.f;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) xr[q][k][b] = v[k];
-        } else {
+        for (int q = 0; q < CH; ++q)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
-        }
+          for (int k = 0; k < 8; ++k) ss = fmaf(xr[q][k][b], xr[q][k][b], ss);
+        ss = warp_sum(ss);
+        if (lane == 0) s_ss[gw][b] = ss;
+      }
+      if (gt < n_p1) s_b1[gt] = lw.p_b1 ? WT<T>::to_float(lw.p_b1, c + gt * P) : 0.f;
+      up_sync();
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float ss = 0.f;
+#pragma unroll
+        for (int w = 0; w < kGroupWarps; ++w) ss += s_ss[w][b];
+        sc[b] = p.rmsnorm ? rsqrtf(ss / (float)d + 1e-6f) : 1.f;
+      }
+    } else {
+      // down group: stage this CTA's b2 slice (off the per-stage critical path)
+      for (int i = gt; i < (w1 - w0) * 32; i += kGroup) {
+        const int row = w0 * 32 + i;
+        s_b2[i] = (row < m && lw.p_b2) ? WT<T>::to_float(lw.p_b2, row) : 0.f;
       }
     }
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      float ss = 0.f;
-#pragma unroll
-      for (int q = 0; q < CH; ++q)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) ss = fmaf(xr[q][k][b], xr[q][k][b], ss);
-      ss = warp_sum(ss);
-      if (lane == 0) s_ss[gw][b] = ss;
-    }
-    if (gt < n_p1) s_b1[gt] = p.p_b1 ? WT<T>::to_float(p.p_b1, c + gt * P) : 0.f;
-    up_sync();
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      float ss = 0.f;
-#pragma unroll
-      for (int w = 0; w < kGroupWarps; ++w) ss += s_ss[w][b];
-      sc[b] = p.rmsnorm ? rsqrtf(ss / (float)d + 1e-6f) : 1.f;
-    }
-  } else {
-    // down group: stage this CTA's b2 slice (off the per-stage critical path)
-    for (int i = gt; i < (w1 - w0) * 32; i += kGroup) {
-      const int row = w0 * 32 + i;
-      s_b2[i] = (row < m && p.p_b2) ? WT<T>::to_float(p.p_b2, row) : 0.f;
-    }
-  }
 
-  // ---------------- phase 1 (up group): g = act_p(s P1 x + b1) ----------------
-  if (is_up) {
-    for (int st = 0; st < st_p1; ++st) {
-      const uint32_t it = st;
-      const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
-      wait_full(it);
-      const uint8_t *buf = stage_ptr(it);
-      float acc[RPM * B];
+    // ---------------- phase 1 (up group): g = act_p(s P1 x + b1) ----------------
+    if (is_up) {
+      for (int st = 0; st < st_p1; ++st) {
+        const uint32_t it = ring + st;
+        const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
+        wait_full(it);
+        const uint8_t *buf = stage_ptr(it);
+        float acc[RPM * B];
 #pragma unroll
-      for (int i = 0; i < RPM * B; ++i) acc[i] = 0.f;
+        for (int i = 0; i < RPM * B; ++i) acc[i] = 0.f;
 #pragma unroll
-      for (int k = 0; k < RPM; ++k) {
+        for (int k = 0; k < RPM; ++k) {
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
-          float wf[8];
-          WT<T>::unpack(lds128z(buf, (size_t)k * row_dn + (size_t)ch * 16, k < kn && ch < chunks), wf);
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
-        }
-      }
-      float *rb = red + (it & 1) * kGroupWarps * kRedStride;
-      up_partials<RPM * B>(acc, rb);
-      if (gt == 0) mbar_arrive_cnt(&empty[it % NS], kConsumerWarps);  // every up warp has read the stage
-      if (gt < kn * B) {
-        const int k = gt / B, b = gt % B;
-        const int j = c + (k0 + k) * P;
-        float u = up_total(rb, gt) * sc[b] + s_b1[k0 + k];
-        if (p.pred_relu) u = fmaxf(u, 0.f);
-        p.g[(size_t)b * r + j] = u;
-      }
-    }
-  }
-  if (trace && tid == 0) trace[1] = globaltimer();
-  grid_sync(p.bar, P);
-  if (trace && tid == 0) trace[2] = globaltimer();
-
-  // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
-  {
-    P2Ctx ctx{stages, full, empty, zbuf, s_b2, &s_count, trace, NS, SB, st_p1, st_p2, w0, w1, m, r, p.words,
-              p.words_p2, p.wcap * 32, p.t, p.g, p.mask, p.uni};
-    const int cg = ((r >> 3) + 31) / 32;
-    if (cg <= 1) p2_phase<T, B, 1>(ctx);
-    else if (cg == 2) p2_phase<T, B, 2>(ctx);
-    else if (cg == 3) p2_phase<T, B, 3>(ctx);
-    else p2_phase<T, B, 4>(ctx);
-  }
-  consumers_sync();
-  if (tid == 0) p.counts[c] = s_count;
-  grid_sync(p.bar, P);
-  if (trace && tid == 0) trace[4] = globaltimer();
-
-  // ---------------- phase 3: compaction of my share ----------------
-  if (warp == 0) {
-    // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
-    constexpr int KPL = 8;  // counts per lane (P <= 256)
-    int cv[KPL];
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) {
-      const int b = lane * KPL + i;
-      cv[i] = (b < P) ? __ldcg(p.counts + b) : 0;
-    }
-    int lsum = 0;
-#pragma unroll
-    for (int i = 0; i < KPL; ++i) lsum += cv[i];
-    int incl = lsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const int n = __shfl_sync(0xffffffffu, incl, 31);
-    const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
-    if (k0 < k1) {
-      int pos = incl - lsum, cand = -1, cand_before = 0;
-#pragma unroll
-      for (int i = 0; i < KPL; ++i) {
-        if (cand < 0 && pos + cv[i] > k0) {
-          cand = lane * KPL + i;
-          cand_before = pos;
-        }
-        pos += cv[i];
-      }
-      const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
-      const int src = __ffs(hit) - 1;
-      const int blk = __shfl_sync(0xffffffffu, cand, src);
-      int before = __shfl_sync(0xffffffffu, cand_before, src);
-      // walk union words from the start of block blk; keep ids with position in [k0, k1)
-      int w = (int)(((int64_t)blk * p.words) / P);
-      while (before < k1 && w < p.words) {
-        const int ww = w + lane;
-        const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
-        uint32_t bitsb[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b)
-          bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
-        const int cnt = __popc(u);
-        int wincl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, wincl, o);
-          if (lane >= o) wincl += t;
-        }
-        int my_pos = before + wincl - cnt;
-        uint32_t v = u;
-        while (v) {
-          const int bit = __ffs(v) - 1;
-          v &= v - 1;
-          if (my_pos >= k0 && my_pos < k1) {
-            const int slot = my_pos - k0;
-            s_ids[slot] = ww * 32 + bit;
-            uint8_t tb = 0;
-#pragma unroll
-            for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
-            s_bits[slot] = tb;
-          }
-          ++my_pos;
-        }
-        before += __shfl_sync(0xffffffffu, wincl, 31);
-        w += 32;
-      }
-    }
-    if (lane == 0) {
-      s_n = n;
-      s_k0 = k0;
-      s_k1 = k1;
-    }
-  }
-  consumers_sync();
-  if (tid == 0) mbar_arrive(ids_ready);  // producer may stream the FFN rows
-  if (trace && tid == 0) trace[5] = globaltimer();
-  const int k0 = s_k0, n_mine = s_k1 - s_k0;
-  for (int k = tid; k < n_mine; k += kConsumers) {
-    const int i = s_ids[k];
-    s_bup[k] = p.b_up ? WT<T>::to_float(p.b_up, i) : 0.f;
-    if (p.ids_out) p.ids_out[k0 + k] = i;
-  }
-  if (p.n_out && c == 0 && tid == 0) *p.n_out = s_n;
-  consumers_sync();
-
-  // ---------------- phase 3: the sparse FFN ----------------
-  const uint32_t it_ffn = st_p1 + st_p2;
-  const int n_st = (n_mine + G - 1) / G;
-  if (is_up) {
-    constexpr int NV = NA * B * (REGLU ? 2 : 1);
-    for (int f = 0; f < n_st; ++f) {
-      const uint32_t it = it_ffn + f;
-      const int kk = f * G, kn = min(G, n_mine - kk);
-      wait_full(it);
-      const uint8_t *buf = stage_ptr(it);
-      float acc[NV];
-#pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] = 0.f;
-#pragma unroll
-      for (int g = 0; g < NA; ++g) {
-        const size_t go = (size_t)g * nb;
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
-          const bool ok = g < kn && ch < chunks;
-          float wu[8];
-          if (REGLU) {
-            float wg[8];
-            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
-            WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            float wf[8];
+            WT<T>::unpack(lds128z(buf, (size_t)k * row_dn + (size_t)ch * 16, k < kn && ch < chunks), wf);
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
-          } else {
-            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
+              for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
           }
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-              acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
-            }
         }
-      }
-      float *rb = red + (f & 1) * kGroupWarps * kRedStride;
-      up_partials<NV>(acc, rb);
-      if (warp == 0) {
-        if (lane < kn * B) {
-          const int g = lane / B, b = lane % B;
-          const int slot = kk + g;
-          const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + s_bup[slot];
-          float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
-          hs[(it % NS) * (NA * B) + lane] = ((s_bits[slot] >> b) & 1) ? hv : 0.f;
+        float *rb = red + (st & 1) * kGroupWarps * kRedStride;
+        up_partials<RPM * B>(acc, rb);
+        if (gt == 0) {
+          mbar_arrive(&hready[it % NS]);                        // keep hready phases = ring uses
+          mbar_arrive_cnt(&empty[it % NS], kConsumerWarps);     // every up warp has read the stage
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&hready[it % NS]);
-      }
-    }
-  } else {
-    float yr[CH][8][B];
-#pragma unroll
-    for (int q = 0; q < CH; ++q)
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-#pragma unroll
-        for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
-    for (int f = 0; f < n_st; ++f) {
-      const uint32_t it = it_ffn + f;
-      const int kn = min(G, n_mine - f * G);
-      wait_full(it);
-      mbar_wait(&hready[it % NS], (f / NS) & 1);
-      const uint8_t *buf = stage_ptr(it);
-      const float *hh = hs + (it % NS) * (NA * B);
-#pragma unroll
-      for (int g = 0; g < NA; ++g) {
-        float h[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
-        const size_t go = (size_t)g * nb + row_up;
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
-          float wf[8];
-          WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
-    }
-    // partial y of this CTA -> global
-#pragma unroll
-    for (int q = 0; q < CH; ++q) {
-      const int ch = gt + q * kGroup;
-      if (ch < chunks) {
-#pragma unroll
-        for (int b = 0; b < B; ++b) {
-          float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
-          __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
-          __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
+        if (gt < kn * B) {
+          const int k = gt / B, b = gt % B;
+          const int j = c + (k0 + k) * P;
+          float u = up_total(rb, gt) * sc[b] + s_b1[k0 + k];
+          if (p.pred_relu) u = fmaxf(u, 0.f);
+          p.g[(size_t)b * r + j] = u;
         }
       }
     }
-  }
+    if (tr && tid == 0) tr[1] = globaltimer();
+    grid_sync(p.bar, P);
+    if (tr && tid == 0) tr[2] = globaltimer();
 
-  if (trace && tid == 0) trace[6] = globaltimer();
-  grid_sync(p.bar, P);
-  if (trace && tid == 0) trace[7] = globaltimer();
-
-  // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
-  {
-    const int j0 = (int)(((int64_t)c * d) / P), j1 = (int)(((int64_t)(c + 1) * d) / P);
-    const int ncol = j1 - j0;
-    constexpr int SPL = 8;    // partial groups summed separately, then combined in order
-    constexpr int PPG = 32;   // partials per group (P <= 256)
-    float *part = reinterpret_cast<float *>(stages);  // every stage is consumed: reuse the ring
-    const int items = ncol * B;
-    for (int idx = tid; idx < items * SPL; idx += kConsumers) {
-      const int sgp = idx / items, it2 = idx % items;
-      const int b = it2 / ncol, j = j0 + it2 % ncol;
-      const int c0 = (sgp * P) / SPL, c1 = ((sgp + 1) * P) / SPL;
-      float v[PPG];
-#pragma unroll
-      for (int q = 0; q < PPG; ++q) v[q] = (c0 + q < c1) ? __ldcg(p.ypart + ((size_t)(c0 + q) * B + b) * d + j) : 0.f;
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < PPG; ++q) acc += v[q];
-      part[sgp * items + it2] = acc;
+    // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
+    {
+      P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
+                r, p.words, p.words_p2, p.wcap * 32, lw.t, p.g, p.mask, p.uni};
+      const int cg = ((r >> 3) + 31) / 32;
+      if (cg <= 1) p2_phase<T, B, 1>(ctx);
+      else if (cg == 2) p2_phase<T, B, 2>(ctx);
+      else if (cg == 3) p2_phase<T, B, 3>(ctx);
+      else p2_phase<T, B, 4>(ctx);
     }
     consumers_sync();
-    for (int it2 = tid; it2 < items; it2 += kConsumers) {
-      const int b = it2 / ncol, j = j0 + it2 % ncol;
-      float acc = 0.f;
+    if (tid == 0) p.counts[c] = s_count;
+    grid_sync(p.bar, P);
+    if (tr && tid == 0) tr[4] = globaltimer();
+
+    // ---------------- phase 3: compaction of my share ----------------
+    if (warp == 0) {
+      // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
+      constexpr int KPL = 8;  // counts per lane (P <= 256)
+      int cv[KPL];
 #pragma unroll
-      for (int sgp = 0; sgp < SPL; ++sgp) acc += part[sgp * items + it2];
-      if (p.b_down) acc += WT<T>::to_float(p.b_down, j);
-      p.y[(size_t)b * d + j] = acc;
+      for (int i = 0; i < KPL; ++i) {
+        const int b = lane * KPL + i;
+        cv[i] = (b < P) ? __ldcg(p.counts + b) : 0;
+      }
+      int lsum = 0;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) lsum += cv[i];
+      int incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int n = __shfl_sync(0xffffffffu, incl, 31);
+      const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
+      if (k0 < k1) {
+        int pos = incl - lsum, cand = -1, cand_before = 0;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) {
+          if (cand < 0 && pos + cv[i] > k0) {
+            cand = lane * KPL + i;
+            cand_before = pos;
+          }
+          pos += cv[i];
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
+        const int src = __ffs(hit) - 1;
+        const int blk = __shfl_sync(0xffffffffu, cand, src);
+        int before = __shfl_sync(0xffffffffu, cand_before, src);
+        // walk union words from the start of block blk; keep ids with position in [k0, k1)
+        int w = (int)(((int64_t)blk * p.words) / P);
+        while (before < k1 && w < p.words) {
+          const int ww = w + lane;
+          const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
+          uint32_t bitsb[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+            bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
+          const int cnt = __popc(u);
+          int wincl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wincl, o);
+            if (lane >= o) wincl += t;
+          }
+          int my_pos = before + wincl - cnt;
+          uint32_t v = u;
+          while (v) {
+            const int bit = __ffs(v) - 1;
+            v &= v - 1;
+            if (my_pos >= k0 && my_pos < k1) {
+              const int slot = my_pos - k0;
+              s_ids[slot] = ww * 32 + bit;
+              uint8_t tb = 0;
+#pragma unroll
+              for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
+              s_bits[slot] = tb;
+            }
+            ++my_pos;
+          }
+          before += __shfl_sync(0xffffffffu, wincl, 31);
+          w += 32;
+        }
+      }
+      if (lane == 0) {
+        s_n = n;
+        s_k0 = k0;
+        s_k1 = k1;
+      }
     }
+    consumers_sync();
+    if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
+    if (tr && tid == 0) tr[5] = globaltimer();
+    const int k0 = s_k0, n_mine = s_k1 - s_k0;
+    for (int k = tid; k < n_mine; k += kConsumers) {
+      const int i = s_ids[k];
+      s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
+      if (p.ids_out) p.ids_out[k0 + k] = i;
+    }
+    if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
+    consumers_sync();
+
+    // ---------------- phase 3: the sparse FFN ----------------
+    const uint32_t it_ffn = ring + st_p1 + st_p2;
+    const int n_st = (n_mine + G - 1) / G;
+    if (is_up) {
+      constexpr int NV = NA * B * (REGLU ? 2 : 1);
+      for (int f = 0; f < n_st; ++f) {
+        const uint32_t it = it_ffn + f;
+        const int kk = f * G, kn = min(G, n_mine - kk);
+        wait_full(it);
+        const uint8_t *buf = stage_ptr(it);
+        float acc[NV];
+#pragma unroll
+        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+#pragma unroll
+        for (int g = 0; g < NA; ++g) {
+          const size_t go = (size_t)g * nb;
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            const bool ok = g < kn && ch < chunks;
+            float wu[8];
+            if (REGLU) {
+              float wg[8];
+              WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
+              WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+            } else {
+              WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+                acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+              }
+          }
+        }
+        float *rb = red + (f & 1) * kGroupWarps * kRedStride;
+        up_partials<NV>(acc, rb);
+        if (warp == 0) {
+          if (lane < kn * B) {
+            const int g = lane / B, b = lane % B;
+            const int slot = kk + g;
+            const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + s_bup[slot];
+            float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
+            hs[(it % NS) * (NA * B) + lane] = ((s_bits[slot] >> b) & 1) ? hv : 0.f;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hready[it % NS]);
+        }
+      }
+    } else {
+      float yr[CH][8][B];
+#pragma unroll
+      for (int q = 0; q < CH; ++q)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+#pragma unroll
+          for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
+      for (int f = 0; f < n_st; ++f) {
+        const uint32_t it = it_ffn + f;
+        const int kn = min(G, n_mine - f * G);
+        wait_full(it);
+        mbar_wait(&hready[it % NS], (it / NS) & 1);
+        const uint8_t *buf = stage_ptr(it);
+        const float *hh = hs + (it % NS) * (NA * B);
+#pragma unroll
+        for (int g = 0; g < NA; ++g) {
+          float h[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
+          const size_t go = (size_t)g * nb + row_up;
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            float wf[8];
+            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
+      }
+      // partial y of this CTA -> global
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int ch = gt + q * kGroup;
+        if (ch < chunks) {
+#pragma unroll
+          for (int b = 0; b < B; ++b) {
+            float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
+            __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
+            __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
+          }
+        }
+      }
+    }
+    ring = it_ffn + n_st;
+
+    if (tr && tid == 0) tr[6] = globaltimer();
+    grid_sync(p.bar, P);
+    if (tr && tid == 0) tr[7] = globaltimer();
+
+    // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
+    {
+      const int j0 = (int)(((int64_t)c * d) / P), j1 = (int)(((int64_t)(c + 1) * d) / P);
+      const int ncol = j1 - j0;
+      constexpr int SPL = 8;    // partial groups summed separately, then combined in order
+      constexpr int PPG = 32;   // partials per group (P <= 256)
+      float *part = s_part;     // [SPL][ncol*B]
+      const int items = ncol * B;
+      for (int idx = tid; idx < items * SPL; idx += kConsumers) {
+        const int sgp = idx / items, it2 = idx % items;
+        const int b = it2 / ncol, j = j0 + it2 % ncol;
+        const int c0 = (sgp * P) / SPL, c1 = ((sgp + 1) * P) / SPL;
+        float v[PPG];
+#pragma unroll
+        for (int q = 0; q < PPG; ++q) v[q] = (c0 + q < c1) ? __ldcg(p.ypart + ((size_t)(c0 + q) * B + b) * d + j) : 0.f;
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < PPG; ++q) acc += v[q];
+        part[sgp * items + it2] = acc;
+      }
+      consumers_sync();
+      for (int it2 = tid; it2 < items; it2 += kConsumers) {
+        const int b = it2 / ncol, j = j0 + it2 % ncol;
+        float acc = 0.f;
+#pragma unroll
+        for (int sgp = 0; sgp < SPL; ++sgp) acc += part[sgp * items + it2];
+        if (lw.b_down) acc += WT<T>::to_float(lw.b_down, j);
+        yout[(size_t)b * d + j] = acc;
+      }
+    }
+    if (tr && tid == 0) tr[8] = globaltimer();
+    if (l < L - 1) grid_sync(p.bar, P);   // the next layer reads all of y
   }
-  if (trace && tid == 0) trace[8] = globaltimer();
 }
 
 // ---------------------------------------------------------------------------
@@ -821,8 +848,10 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.wcap = (words_all + w.P - 1) / w.P + 1;
   const size_t extra = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
                        (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 +
-                       (size_t)w.idcap * 9 + 256;
-  w.smem = (int)((size_t)w.NS * sb + extra);
+                       (size_t)w.idcap * 9;
+  w.part_off = (int)(((size_t)w.NS * sb + extra + 15) / 16 * 16);
+  const int pcap = (d + w.P - 1) / w.P + 1;
+  w.smem = w.part_off + 8 * pcap * kFusedMaxB * 4 + 64;
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, 64)) return false;
   if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
@@ -830,6 +859,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   if (!alloc((void **)&w.counts, (size_t)w.P * 4)) return false;
   if (!alloc((void **)&w.mask, (size_t)maxB * words * 4)) return false;
   if (!alloc((void **)&w.uni, (size_t)words * 4)) return false;
+  if (!alloc((void **)&w.xbuf, (size_t)std::min(maxB, kFusedMaxB) * d * 4)) return false;
+  if (w.smem > 227 * 1024) return true;
   w.enabled = true;
   return true;
 }
@@ -877,25 +908,28 @@ inline cudaError_t fused_launch_t(FusedWork &w, const FusedParams &prm, cudaStre
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-template <typename T>
-inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*/, cudaStream_t s) {
+// Parameters shared by the single-layer and the stack launch.
+inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   FusedParams p{};
-  p.w_up = (const uint8_t *)a.w_up;
-  p.w_down = (const uint8_t *)a.w_down;
-  p.p_w1 = (const uint8_t *)a.p_w1;
-  p.p_w2 = (const uint8_t *)a.p_w2;
-  p.b_up = a.b_up;
-  p.b_down = a.b_down;
-  p.p_b1 = a.p_b1;
-  p.p_b2 = a.p_b2;
+  p.lw0.w_up = (const uint8_t *)a.w_up;
+  p.lw0.w_down = (const uint8_t *)a.w_down;
+  p.lw0.p_w1 = (const uint8_t *)a.p_w1;
+  p.lw0.p_w2 = (const uint8_t *)a.p_w2;
+  p.lw0.b_up = a.b_up;
+  p.lw0.b_down = a.b_down;
+  p.lw0.p_b1 = a.p_b1;
+  p.lw0.p_b2 = a.p_b2;
+  p.lw0.t = a.threshold;
+  p.lws = nullptr;
+  p.L = 1;
   p.x = a.x;
   p.y = a.y;
+  p.xbuf = w.xbuf;
   p.d = a.d;
   p.m = a.m;
   p.r = a.r;
   p.words = a.words;
   p.B = a.B;
-  p.t = a.threshold;
   p.rmsnorm = a.rmsnorm;
   p.pred_relu = a.pred_relu;
   p.mask = a.mask_out ? a.mask_out : w.mask;
@@ -911,14 +945,20 @@ inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*
   p.words_p2 = w.words_p2;
   p.idcap = w.idcap;
   p.wcap = w.wcap;
+  p.part_off = w.part_off;
   p.trace = w.trace;
+  return p;
+}
+
+template <typename T>
+inline cudaError_t fused_launch_p(FusedWork &w, FusedParams p, bool reglu, int B, cudaStream_t s) {
   int NA, G, RP1;
-  fused_geometry(w, a.d, a.reglu, &NA, &G, &RP1);
+  fused_geometry(w, p.d, reglu, &NA, &G, &RP1);
   p.G = G;
   p.rows_p1 = RP1;
-  const int CH = fused_ch(a.d);
+  const int CH = fused_ch(p.d);
 #define PI_FL(NB, RG, CHV, NAV) \
-  if (a.B == NB && a.reglu == RG && CH == CHV && NA == NAV) return fused_launch_t<T, NB, RG, CHV, NAV>(w, p, s);
+  if (B == NB && reglu == RG && CH == CHV && NA == NAV) return fused_launch_t<T, NB, RG, CHV, NAV>(w, p, s);
 #define PI_FL_RG(NB, RG)                                                                       \
   PI_FL(NB, RG, 1, 8) PI_FL(NB, RG, 1, 1) PI_FL(NB, RG, 2, 8) PI_FL(NB, RG, 2, 1) PI_FL(NB, RG, 3, 1) \
   PI_FL(NB, RG, 4, 1)
@@ -927,6 +967,25 @@ inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*
 #undef PI_FL_RG
 #undef PI_FL
   return cudaErrorNotSupported;
+}
+
+// one layer
+template <typename T>
+inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*/, cudaStream_t s) {
+  return fused_launch_p<T>(w, fused_params(w, a), a.reglu, a.B, s);
+}
+
+// L chained layers in one launch: a describes layer 0 (shapes, x, y); lws is a device array of
+// the L layers' weights; n_out (optional) receives the L union counts.
+template <typename T>
+inline cudaError_t fused_launch_stack(FusedWork &w, const FusedArgs &a, const LayerW *lws, int L,
+                                      cudaStream_t s) {
+  FusedParams p = fused_params(w, a);
+  p.lws = lws;
+  p.L = L;
+  p.mask = w.mask;
+  p.ids_out = nullptr;
+  return fused_launch_p<T>(w, p, a.reglu, a.B, s);
 }
 
 }  // namespace pi

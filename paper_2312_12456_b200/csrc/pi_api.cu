@@ -322,6 +322,120 @@ extern "C" pi_status pi_layer_destroy(pi_layer *L) {
   return PI_OK;
 }
 
+static pi_status stack_dev(pi_layer *const *layers, int32_t n_layers, const float *x, int32_t B, float *y,
+                           int32_t *n_out, cudaStream_t s);
+
+static pi_status check_common(const pi_layer *L, int B);
+
+// ---------------------------------------------------------------------------
+// stacks: one persistent launch for L layers
+// ---------------------------------------------------------------------------
+struct pi_stack {
+  std::vector<pi_layer *> layers;
+  LayerW *lws = nullptr;  // device [L]
+  bool fused = false;
+};
+
+extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, pi_stack **out) {
+  g_err.clear();
+  if (!out) return fail(PI_ERR_INVALID_ARGUMENT, "stack: out is NULL");
+  *out = nullptr;
+  if (!layers || n_layers < 1) return fail(PI_ERR_INVALID_ARGUMENT, "stack: NULL layers or n_layers < 1");
+  const pi_layer *L0 = layers[0];
+  if (!L0) return fail(PI_ERR_INVALID_ARGUMENT, "stack: layer 0 is NULL");
+  for (int l = 0; l < n_layers; ++l) {
+    const pi_layer *Ll = layers[l];
+    if (!Ll) return fail(PI_ERR_INVALID_ARGUMENT, "stack: layer %d is NULL", l);
+    if (Ll->d != L0->d || Ll->m_local != L0->m_local || Ll->r != L0->r || Ll->act != L0->act ||
+        Ll->dtype != L0->dtype || Ll->pred_act != L0->pred_act || Ll->flags != L0->flags ||
+        Ll->max_batch != L0->max_batch || Ll->device != L0->device)
+      return fail(PI_ERR_SHAPE, "stack: layer %d (id %d) differs from layer 0 in shape/dtype/act/flags", l,
+                  Ll->layer_id);
+  }
+  pi_stack *S = new pi_stack();
+  S->layers.assign(layers, layers + n_layers);
+  S->fused = !(L0->flags & PI_FLAG_MULTI_KERNEL) && L0->fw.enabled;
+  std::vector<LayerW> h(n_layers);
+  for (int l = 0; l < n_layers; ++l) {
+    const pi_layer *Ll = layers[l];
+    h[l].w_up = (const uint8_t *)Ll->w_up;
+    h[l].w_down = (const uint8_t *)Ll->w_down;
+    h[l].p_w1 = (const uint8_t *)Ll->p_w1;
+    h[l].p_w2 = (const uint8_t *)Ll->p_w2;
+    h[l].b_up = Ll->b_up;
+    h[l].b_down = Ll->b_down;
+    h[l].p_b1 = Ll->p_b1;
+    h[l].p_b2 = Ll->p_b2;
+    h[l].t = Ll->threshold;
+    h[l].pad = 0;
+  }
+  if (cudaMalloc(&S->lws, sizeof(LayerW) * n_layers) != cudaSuccess) {
+    delete S;
+    return fail(PI_ERR_OUT_OF_MEMORY, "stack: layer table");
+  }
+  if (cudaMemcpy(S->lws, h.data(), sizeof(LayerW) * n_layers, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(S->lws);
+    delete S;
+    return fail(PI_ERR_CUDA, "stack: layer table copy");
+  }
+  *out = S;
+  return PI_OK;
+}
+
+extern "C" pi_status pi_stack_destroy(pi_stack *S) {
+  g_err.clear();
+  if (!S) return PI_OK;
+  cudaDeviceSynchronize();
+  cudaFree(S->lws);
+  delete S;
+  return PI_OK;
+}
+
+static pi_status stack_run_dev(pi_stack *S, const float *x, int B, float *y, int32_t *n_out, cudaStream_t s) {
+  pi_layer *L0 = S->layers[0];
+  const int n = (int)S->layers.size();
+  if (S->fused && fused_supported(L0->fw, B)) {
+    return dispatch_t(L0->dtype, [&](auto tt) {
+      using T = typename decltype(tt)::type;
+      FusedArgs a{};
+      a.x = x; a.y = y; a.d = L0->d; a.m = L0->m_local; a.r = L0->r; a.words = L0->words; a.B = B;
+      a.threshold = L0->threshold; a.rmsnorm = (L0->flags & PI_FLAG_INPUT_RMSNORM) != 0;
+      a.pred_relu = L0->pred_act == PI_PRED_RELU; a.reglu = L0->act == PI_ACT_REGLU;
+      a.n_out = n_out;
+      cudaError_t e = fused_launch_stack<T>(L0->fw, a, S->lws, n, s);
+      if (e != cudaSuccess) return fail(PI_ERR_CUDA, "stack: fused launch: %s", cudaGetErrorString(e));
+      return PI_OK;
+    });
+  }
+  return stack_dev(S->layers.data(), n, x, B, y, n_out, s);
+}
+
+extern "C" pi_status pi_stack_run(pi_stack *S, const float *x, int32_t B, float *y, int32_t *n_active_out,
+                                  pi_stream_t stream) {
+  g_err.clear();
+  if (!S) return fail(PI_ERR_INVALID_ARGUMENT, "stack handle is NULL");
+  if (!x || !y) return fail(PI_ERR_INVALID_ARGUMENT, "stack: NULL x or y");
+  PI_TRY(check_common(S->layers[0], B));
+  if (!aligned16(x) || !aligned16(y)) return fail(PI_ERR_ALIGNMENT, "stack: x and y must be 16-B aligned");
+  return stack_run_dev(S, x, B, y, n_active_out, (cudaStream_t)stream);
+}
+
+extern "C" pi_status pi_stack_run_host(pi_stack *S, const float *x_host, int32_t B, float *y_host,
+                                       pi_stream_t stream) {
+  g_err.clear();
+  if (!S) return fail(PI_ERR_INVALID_ARGUMENT, "stack handle is NULL");
+  if (!x_host || !y_host) return fail(PI_ERR_INVALID_ARGUMENT, "stack: NULL x_host or y_host");
+  PI_TRY(check_common(S->layers[0], B));
+  cudaStream_t s = (cudaStream_t)stream;
+  pi_layer *L0 = S->layers[0];
+  const size_t bytes = (size_t)B * L0->d * 4;
+  PI_CUDA(cudaMemcpyAsync(L0->hx, x_host, bytes, cudaMemcpyHostToDevice, s));
+  PI_TRY(stack_run_dev(S, L0->hx, B, L0->hy, nullptr, s));
+  PI_CUDA(cudaMemcpyAsync(y_host, L0->hy, bytes, cudaMemcpyDeviceToHost, s));
+  PI_CUDA(cudaStreamSynchronize(s));
+  return PI_OK;
+}
+
 extern "C" pi_status pi_layer_set_trace(pi_layer *L, uint64_t *dev_buf) {
   g_err.clear();
   if (!L) return fail(PI_ERR_INVALID_ARGUMENT, "layer handle is NULL");

@@ -34,7 +34,8 @@ PI_MAX_BATCH = 8
 
 EXPORTS = ("pi_version", "pi_last_error", "pi_layer_create", "pi_layer_destroy", "pi_layer_get_info",
            "pi_predict", "pi_compact", "pi_sparse_ffn", "pi_layer_forward", "pi_layer_forward_host",
-           "pi_stack_forward", "pi_stack_forward_host", "pi_partition", "pi_layer_set_trace")
+           "pi_stack_forward", "pi_stack_forward_host", "pi_partition", "pi_layer_set_trace",
+           "pi_stack_create", "pi_stack_destroy", "pi_stack_run", "pi_stack_run_host")
 
 
 class PiError(RuntimeError):
@@ -84,6 +85,10 @@ def _load() -> ctypes.CDLL:
     lib.pi_stack_forward_host.argtypes = [P(vp), i32, vp, i32, vp, vp]
     lib.pi_partition.argtypes = [vp, i32, i32, i32, vp, vp, vp]
     lib.pi_layer_set_trace.argtypes = [vp, vp]
+    lib.pi_stack_create.argtypes = [P(vp), i32, P(vp)]
+    lib.pi_stack_destroy.argtypes = [vp]
+    lib.pi_stack_run.argtypes = [vp, vp, i32, vp, vp, vp]
+    lib.pi_stack_run_host.argtypes = [vp, vp, i32, vp, vp]
     for name in EXPORTS:
         if name not in ("pi_version", "pi_last_error"):
             getattr(lib, name).restype = ctypes.c_int
@@ -236,6 +241,41 @@ def pi_stack_forward_host(layers, x_host: torch.Tensor, y_host: torch.Tensor, st
     assert not x_host.is_cuda and not y_host.is_cuda
     _check(_lib.pi_stack_forward_host(arr, len(arr), x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
                                       _stream(stream)))
+
+
+class StackHandle:
+    """Owns a pi_stack (one persistent launch per decode step for all layers)."""
+
+    def __init__(self, layers: Sequence[Layer]):
+        self.layers = list(layers)       # keep the layers alive while the stack exists
+        arr = handles(self.layers)
+        h = ctypes.c_void_p()
+        _check(_lib.pi_stack_create(arr, len(arr), ctypes.byref(h)))
+        self.handle = h
+
+    def run(self, x, y, n_active_out=None, stream=None):
+        _check(_lib.pi_stack_run(self.handle, _ptr(x), x.shape[0], _ptr(y), _ptr(n_active_out), _stream(stream)))
+
+    def run_host(self, x_host: torch.Tensor, y_host: torch.Tensor, stream=None):
+        assert not x_host.is_cuda and not y_host.is_cuda
+        _check(_lib.pi_stack_run_host(self.handle, x_host.data_ptr(), x_host.shape[0], y_host.data_ptr(),
+                                      _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None:
+            _lib.pi_stack_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+pi_stack_create = StackHandle
+pi_stack_run = StackHandle.run
+pi_stack_run_host = StackHandle.run_host
 
 
 def pi_partition(freq, n_shards: int, granule: int = 1):

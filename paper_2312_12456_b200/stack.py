@@ -48,6 +48,8 @@ class Stack:
         self.group = group
         self.handles = pi.handles(layers)
         self.d = layers[0].d
+        # world 1: one persistent launch per step for all layers (pi_stack_run)
+        self.stack = pi.StackHandle(layers) if world == 1 else None
 
     def __len__(self):
         return len(self.layers)
@@ -57,7 +59,7 @@ class Stack:
         """One decode step for B tokens through every layer.  World size 1: one pi_stack_forward
         call.  World size > 1: per layer pi_layer_forward on the local shard, then all-reduce."""
         if self.world == 1:
-            pi.pi_stack_forward(self.handles, x, y, n_out)
+            self.stack.run(x, y, n_out)
             return y
         cur = x
         for l, L in enumerate(self.layers):
@@ -68,6 +70,9 @@ class Stack:
         return y
 
     def close(self):
+        if self.stack is not None:
+            self.stack.close()
+            self.stack = None
         for L in self.layers:
             L.close()
 

@@ -133,4 +133,8 @@ def test_null_handles(pi):
     assert lib.pi_stack_forward(None, 0, None, 1, None, None, None) == 1
     assert lib.pi_stack_forward_host(None, 0, None, 1, None, None) == 1
     assert lib.pi_layer_set_trace(None, None) == 1
+    assert lib.pi_stack_create(None, 1, None) == 1
+    assert lib.pi_stack_destroy(None) == 0
+    assert lib.pi_stack_run(None, None, 1, None, None, None) == 1
+    assert lib.pi_stack_run_host(None, None, 1, None, None) == 1
     assert "NULL" in lib.pi_last_error().decode()

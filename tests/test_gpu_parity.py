@@ -414,3 +414,40 @@ def test_full_size_layers(env, name):
     assert 0.03 < act < 0.3, act
     del L, w
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name,dims,B", [("c4", (2048, 3000, 64), 1), ("c3", (1024, 2000, 64), 2),
+                                         ("c1", (768, 3072, 64), 1), ("c5", (12288, 700, 64), 1)])
+def test_stack_kernel_equals_layer_chain(env, name, dims, B):
+    """pi_stack_run (one persistent launch for all layers) == chaining pi_layer_forward, bit for bit,
+    and every layer matches the oracle on its own input."""
+    gen, pi = env
+    cfg = gen.CONFIGS[name]
+    d, m, r = dims
+    flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
+    ws = [gen.make_layer(cfg, layer=l, seed=2, device="cuda", d=d, m=m, r=r) for l in range(4)]
+    Ls = [pi.Layer(w, max_batch=2, flags=flags, layer_id=l) for l, w in enumerate(ws)]
+    S = pi.StackHandle(Ls)
+    x = gen.tokens(B, d, seed=3, device="cuda")
+    y = torch.empty(B, d, device="cuda")
+    n = torch.zeros(4, dtype=torch.int32, device="cuda")
+    S.run(x, y, n)
+    torch.cuda.synchronize()
+    cur = x
+    for l, L in enumerate(Ls):
+        yl, gm, ids, nl = run_forward(pi, L, cur)
+        assert nl == int(n[l].item())
+        oracle_check(ws[l], cur, yl, gm, ids, norm=cfg.rmsnorm)
+        cur = torch.from_numpy(yl).cuda()
+    assert (y.cpu().numpy() == cur.cpu().numpy()).all()
+    # the host-buffer entry point returns the same
+    yh = torch.empty(B, d).pin_memory()
+    S.run_host(x.cpu().pin_memory(), yh)
+    assert (yh.numpy() == y.cpu().numpy()).all()
+    # repeated runs are bitwise identical (fixed reduction order)
+    for _ in range(3):
+        y2 = torch.empty_like(y)
+        S.run(x, y2)
+        torch.cuda.synchronize()
+        assert torch.equal(y2, y)
+    S.close()
