@@ -262,6 +262,7 @@ struct P2Ctx {
   int *s_count;
   unsigned long long *trace;
   int NS, SB, st_p1, st_p2, w0, w1, m, r, words, words_p2, zst;
+  uint32_t ring0;
   float t;
   const float *g;
   uint32_t *mask, *uni;
@@ -296,7 +297,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     const int nrows = min(x.m, wb * 32) - wa * 32;
     const int zoff = (wa - x.w0) * 32;   // CTA-local row of this stage's first row
     mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
-    if (x.trace && tid == 0 && it < 56) x.trace[16 + it] = globaltimer();
+    if (x.trace && tid == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
     const uint8_t *buf = x.stages + (size_t)(it % x.NS) * x.SB;
     for (int rb0 = warp * RR; rb0 < nrows; rb0 += kConsumerWarps * RR) {
       float v[NV];
@@ -415,17 +416,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   if (warp == kConsumerWarps) {
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
-    uint32_t it = 0;
+    uint32_t it = 0, trace_it0 = 0xffffffffu;
     auto acquire = [&](uint32_t bytes) -> uint8_t * {
       const int s = it % NS;
       const uint32_t use = it / NS;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
-      if (trace && it < 56) trace[72 + it] = globaltimer();
+      if (trace && it >= trace_it0 && it - trace_it0 < 56) trace[72 + it - trace_it0] = globaltimer();
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
     };
     for (int l = 0; l < L; ++l) {
       const LayerW lw = layer(l);
+      if (l == (L > 1 ? 1 : 0)) trace_it0 = it;
       for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
         const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
         uint8_t *dst = acquire((uint32_t)(kn * row_dn));
@@ -474,12 +476,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     const LayerW lw = layer(l);
     const float *xin = (l == 0) ? p.x : p.xbuf;
     float *yout = (l == L - 1) ? p.y : p.xbuf;
-    unsigned long long *tr = (l == 0) ? trace : nullptr;
+    unsigned long long *tr = (l == (L > 1 ? 1 : 0)) ? trace : nullptr;   // steady-state layer
+    const uint32_t ring0 = ring;
     auto wait_full = [&](uint32_t it) {
       mbar_wait(&full[it % NS], (it / NS) & 1);
-      if (tr && tid == 0 && it < 56) tr[16 + it] = globaltimer();
+      if (tr && tid == 0 && it - ring0 < 56) tr[16 + it - ring0] = globaltimer();
     };
     if (tid == 0) s_count = 0;
+    if (tr && tid == 0) tr[0] = globaltimer();
 
     float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
     float sc[B];
@@ -572,7 +576,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
       P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
-                r, p.words, p.words_p2, p.wcap * 32, lw.t, p.g, p.mask, p.uni};
+                r, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
       const int cg = ((r >> 3) + 31) / 32;
       if (cg <= 1) p2_phase<T, B, 1>(ctx);
       else if (cg == 2) p2_phase<T, B, 2>(ctx);

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--stack", action="store_true", help="trace layer 1 of a pi_stack_run launch")
     a = ap.parse_args()
     cfg = gen.CONFIGS[a.config]
     st, _ = build_stack(cfg, n_layers=min(a.layers, cfg.layers), device="cuda", max_batch=a.batch)
@@ -37,11 +38,19 @@ def main():
     stage_rows = []
     for rep in range(a.reps):
         L = st.layers[rep % len(st.layers)]
+        if a.stack:
+            L = st.layers[0]
         L.set_trace(buf)
         buf.zero_()
-        L.forward(x, y, None, None, n)
+        if a.stack:
+            nn = torch.zeros(len(st.layers), dtype=torch.int32, device="cuda")
+            st.stack.run(x, y, nn)
+        else:
+            L.forward(x, y, None, None, n)
         torch.cuda.synchronize()
         L.set_trace(None)
+        if a.stack:
+            n = nn[1:2]
         full = buf.view(P, 256).cpu().numpy().astype(np.float64)
         t = full[:, :9]
         t0 = t[:, 0].min()
