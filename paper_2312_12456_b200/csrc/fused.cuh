@@ -57,6 +57,7 @@ struct FusedWork {
   int d = 0, m = 0, r = 0;
   bool reglu = false;
   unsigned int *epoch = nullptr;      // launch counter for the exchange tags
+  unsigned long long *ctr = nullptr;  // readiness counters (see FusedParams)
   unsigned long long *g64 = nullptr;  // [maxB, r] tagged
   unsigned long long *yp64 = nullptr; // [P, maxB, d] tagged
   unsigned long long *cnt64 = nullptr;   // [P] tagged
@@ -100,6 +101,7 @@ struct FusedParams {
   unsigned long long *mask64, *uni64, *cnt64;   // tagged mask words, union words, per-CTA counts
   unsigned long long *yp64;   // tagged per-CTA partial outputs [P][B][d]
   unsigned int *epoch;        // launch counter (tags)
+  unsigned long long *ctr;    // readiness counters: [0] g, [16] counts, [32] partials, [48] x, [64] layer sequence
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
 };
@@ -212,6 +214,20 @@ __device__ __forceinline__ void poll_pause(unsigned long long t0) {
   __nanosleep(64);
   if (globaltimer() - t0 > 4000000000ull) __trap();
 }
+// Readiness counters: a CTA that has issued (not necessarily completed) its tagged stores for a
+// phase adds 1; readers wait until the counter reaches the phase's target before loading, so
+// only one thread per CTA polls one word.  No ordering is needed between the stores and the
+// add: the tags make any word that is not yet visible read as stale, and it is simply re-read.
+__device__ __forceinline__ void ctr_add(unsigned long long *ctr) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+}
+__device__ __forceinline__ void ctr_wait(const unsigned long long *ctr, unsigned long long target) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_tagged(ctr) < target) {
+    __nanosleep(32);
+    if (globaltimer() - t0 > 4000000000ull) __trap();
+  }
+}
 
 // Transpose reduction of NV per-lane partials (NV a power of two <= 32): afterwards every
 // lane l holds the warp-wide total of value (l & (NV - 1)).  NV - 1 + log2(32 / NV) shuffles
@@ -281,6 +297,8 @@ struct P2Ctx {
   unsigned long long *mask64, *uni64;
   uint32_t *mask_out;              // plain per-token words for the ABI (single layer) or NULL
   uint32_t tag;
+  const unsigned long long *ctr;   // readiness counter of g
+  unsigned long long target;
 };
 
 template <typename T, int B, int CG>
@@ -294,6 +312,8 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   // g is read by every warp of every CTA: warp 0 fetches it once per CTA (polling the tags
   // until every P1 row of this layer has been published), then it is broadcast via smem
   if (warp == 0) {
+    if (lane == 0) ctr_wait(x.ctr, x.target);
+    __syncwarp();
     const unsigned long long t0 = globaltimer();
     const int nv = B * x.r;
     for (int base = 0; base < nv; base += 32 * 16) {
@@ -442,6 +462,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
   __shared__ uint32_t s_ep;
+  __shared__ unsigned long long s_seq;
   unsigned long long *trace = p.trace ? p.trace + (size_t)c * 256 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
 
@@ -467,9 +488,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     unsigned int e;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(p.epoch) : "memory");
     s_ep = e;
+    s_seq = ld_tagged(p.ctr + 64);
   }
   __syncthreads();
   const uint32_t ep = s_ep;
+  const unsigned long long seq = s_seq;
+  auto target = [&](int l) -> unsigned long long { return (seq + (unsigned long long)l + 1ull) * (unsigned long long)P; };
   auto tag_of = [&](int l) -> uint32_t { return ep * 4096u + (uint32_t)l + 1u; };
 
   // =====================================================================================
@@ -568,7 +592,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           }
         }
       } else {
-        // x_l = y_{l-1}: poll the tagged words the previous layer's reductions published
+        // x_l = y_{l-1}: wait for every CTA's reduction of layer l-1, then read the tagged words
+        if (gt == 0) ctr_wait(p.ctr + 48, target(l - 1));
+        up_sync();
         const uint32_t tprev = tag_of(l - 1);
         const unsigned long long t0 = globaltimer();
 #pragma unroll
@@ -661,12 +687,16 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         }
       }
     }
+    if (is_up) {
+      up_sync();                       // every up thread has issued its g stores
+      if (gt == 0) ctr_add(p.ctr + 0);
+    }
     if (tr && tid == 0) tr[1] = globaltimer();
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
       P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, sg, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
-                r, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g64, p.mask64, p.uni64, p.mask_out, tag};
+                r, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g64, p.mask64, p.uni64, p.mask_out, tag, p.ctr + 0, target(l)};
       const int cg = ((r >> 3) + 31) / 32;
       if (cg <= 1) p2_phase<T, B, 1>(ctx);
       else if (cg == 2) p2_phase<T, B, 2>(ctx);
@@ -674,7 +704,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       else p2_phase<T, B, 4>(ctx);
     }
     consumers_sync();
-    if (tid == 0) st_tagged(p.cnt64 + c, tagged(tag, (uint32_t)s_count));
+    if (tid == 0) {
+      st_tagged(p.cnt64 + c, tagged(tag, (uint32_t)s_count));   // (mask and union words were issued before
+      ctr_add(p.ctr + 16);                                        //  the consumers_sync above)
+    }
     if (tr && tid == 0) tr[2] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
@@ -682,6 +715,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
       constexpr int KPL = 8;  // counts per lane (P <= 256)
       int cv[KPL];
+      if (lane == 0) ctr_wait(p.ctr + 16, target(l));
+      __syncwarp();
       {
         const unsigned long long t0 = globaltimer();
 #pragma unroll
@@ -894,6 +929,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     }
     ring = it_ffn + n_st;
 
+    consumers_sync();                  // every down thread has issued its partial stores
+    if (tid == 0) {
+      ctr_add(p.ctr + 32);
+      ctr_wait(p.ctr + 32, target(l));
+    }
+    consumers_sync();
     if (tr && tid == 0) tr[6] = globaltimer();
 
     // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
@@ -948,10 +989,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         else st_tagged(p.x64 + (size_t)b * d + j, tagged(tag, __float_as_uint(acc)));
       }
     }
+    consumers_sync();   // every x store of this CTA issued; smem of this layer is free
+    if (tid == 0) ctr_add(p.ctr + 48);   // every layer, so the counter stays at (seq + l + 1) P
     if (tr && tid == 0) tr[8] = globaltimer();
-    consumers_sync();   // CTA-local: smem of this layer is free
   }
-  if (c == 0 && tid == 0) atomicAdd(p.epoch, 1u);   // every CTA read the epoch long ago
+  if (c == 0 && tid == 0) {   // every CTA read the epoch and the layer sequence long ago
+    atomicAdd(p.epoch, 1u);
+    st_tagged(p.ctr + 64, seq + (unsigned long long)L);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -992,6 +1037,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const int mb = kFusedMaxB;
   (void)maxB;
   if (!alloc((void **)&w.epoch, 64)) return false;
+  if (!alloc((void **)&w.ctr, 80 * 8)) return false;
   if (!alloc((void **)&w.g64, (size_t)mb * r * 8)) return false;
   if (!alloc((void **)&w.yp64, (size_t)w.P * mb * d * 8)) return false;
   if (!alloc((void **)&w.cnt64, (size_t)w.P * 8)) return false;
@@ -1008,6 +1054,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
 inline void fused_init(FusedWork &w, cudaStream_t s) {
   if (!w.enabled) return;   // tag 0 is never current: zeroed buffers read as "not yet published"
   cudaMemsetAsync(w.epoch, 0, 64, s);
+  cudaMemsetAsync(w.ctr, 0, 80 * 8, s);
   const int mb = kFusedMaxB, words = (w.m + 31) / 32;
   cudaMemsetAsync(w.g64, 0, (size_t)mb * w.r * 8, s);
   cudaMemsetAsync(w.yp64, 0, (size_t)w.P * mb * w.d * 8, s);
@@ -1089,6 +1136,7 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.cnt64 = w.cnt64;
   p.yp64 = w.yp64;
   p.epoch = w.epoch;
+  p.ctr = w.ctr;
   p.NS = w.NS;
   p.stage_bytes = w.stage_bytes;
   p.words_p2 = w.words_p2;
