@@ -56,16 +56,14 @@ struct FusedWork {
   int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0, part_off = 0, pcap = 0;
   int d = 0, m = 0, r = 0;
   bool reglu = false;
-  unsigned int *epoch = nullptr;      // launch counter for the exchange tags
-  unsigned long long *ctr = nullptr;  // readiness counters (see FusedParams)
-  unsigned long long *g64 = nullptr;  // [maxB, r] tagged
-  unsigned long long *yp64 = nullptr; // [P, maxB, d] tagged
-  unsigned long long *cnt64 = nullptr;   // [P] tagged
-  unsigned long long *mask64 = nullptr;  // [maxB, words] tagged
-  unsigned long long *uni64 = nullptr;   // [words] tagged
-  unsigned long long *x64 = nullptr;     // [maxB, d] tagged inter-layer activations (stack launch)
+  unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
+  float *g = nullptr;                 // [maxB, r]
+  float *ypart = nullptr;             // [P, maxB, d]
+  int *counts = nullptr;              // [P]
+  uint32_t *mask = nullptr;           // [maxB, words]
+  uint32_t *uni = nullptr;            // [words]
+  float *xbuf = nullptr;              // [maxB, d] inter-layer activations (stack launch)
   unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
-  size_t ws_bytes = 0;
 };
 
 struct FusedArgs {
@@ -92,16 +90,14 @@ struct FusedParams {
   int L;
   const float *x;             // layer-0 input [B, d]
   float *y;                   // last-layer output [B, d]
-  unsigned long long *x64;    // tagged inter-layer activations [B][d] (stack launch)
+  float *xbuf;                // inter-layer activations [B, d] (stack launch)
   int d, m, r, words, B;
   int rmsnorm, pred_relu;
-  uint32_t *mask_out;         // plain per-token mask words (single layer) or NULL
+  uint32_t *mask, *uni;
   int32_t *ids_out, *n_out;   // n_out: [L] union counts
-  unsigned long long *g64;    // tagged predictor hidden [B][r]
-  unsigned long long *mask64, *uni64, *cnt64;   // tagged mask words, union words, per-CTA counts
-  unsigned long long *yp64;   // tagged per-CTA partial outputs [P][B][d]
-  unsigned int *epoch;        // launch counter (tags)
-  unsigned long long *ctr;    // readiness counters: [0] g, [16] counts, [32] partials, [48] x, [64] layer sequence
+  float *g, *ypart;
+  int *counts;
+  unsigned long long *bar;
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
 };
@@ -183,50 +179,44 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Cross-CTA data exchange without grid barriers.  Every value another CTA must read is
-// published as a 64-bit word (tag << 32 | 32-bit payload) with a relaxed gpu-scope store; a
-// 64-bit access is single-copy atomic, so a reader that sees the expected tag also sees the
-// payload written with it -- no fences, no atomics.  Readers poll (relaxed gpu-scope loads,
-// L1 bypassed) only the words they need until every tag is current, so a CTA waits only for
-// the producers of its own inputs.  tag = launch epoch * 4096 + layer + 1 (never 0); each
-// slot is rewritten every launch, so a stale slot holds the previous tag at most.
-__device__ __forceinline__ unsigned long long tagged(uint32_t tag, uint32_t payload) {
-  return ((unsigned long long)tag << 32) | payload;
-}
-__device__ __forceinline__ void st_tagged(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_tagged2(unsigned long long *p, unsigned long long a, unsigned long long b) {
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_tagged(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void ld_tagged2(const unsigned long long *p, unsigned long long &a, unsigned long long &b) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-__device__ __forceinline__ bool tag_ok(unsigned long long v, uint32_t tag) { return (uint32_t)(v >> 32) == tag; }
-__device__ __forceinline__ float tag_f(unsigned long long v) { return __uint_as_float((uint32_t)v); }
-// back-off between polls + a 4-second watchdog that traps instead of hanging the device
-__device__ __forceinline__ void poll_pause(unsigned long long t0) {
-  __nanosleep(64);
-  if (globaltimer() - t0 > 4000000000ull) __trap();
-}
-// Readiness counters: a CTA that has issued (not necessarily completed) its tagged stores for a
-// phase adds 1; readers wait until the counter reaches the phase's target before loading, so
-// only one thread per CTA polls one word.  No ordering is needed between the stores and the
-// add: the tags make any word that is not yet visible read as stale, and it is simply re-read.
-__device__ __forceinline__ void ctr_add(unsigned long long *ctr) {
-  asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
-}
-__device__ __forceinline__ void ctr_wait(const unsigned long long *ctr, unsigned long long target) {
-  const unsigned long long t0 = globaltimer();
-  while (ld_tagged(ctr) < target) {
-    __nanosleep(32);
-    if (globaltimer() - t0 > 4000000000ull) __trap();
+// Grid barrier over the P co-resident CTAs (cooperative launch).  bar[0] is a monotonic
+// 64-bit arrival counter; bar[16 * (1 + c)] is CTA c's release flag, each on its own 128-byte
+// line.  An arrival that returns `old` belongs to episode e = old / P + 1; the last arrival of
+// the episode writes e into every CTA's flag (warp 0 of that CTA, 32 lanes in parallel), and
+// every CTA polls only its own flag -- no L2 line is polled by 148 SMs at once, so the
+// arrivals are not slowed by the pollers.  A 4-second watchdog traps instead of hanging.
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsigned long long *dbg = nullptr) {
+  consumers_sync();  // every consumer thread of this CTA has issued its global writes
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    unsigned long long old = 0;
+    long long c0 = clock64();
+    if (lane == 0) {
+      if (dbg) dbg[0] = clock64() - c0;
+      asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+      if (dbg) dbg[1] = clock64() - c0 + (old == 0xffffffffffffull ? 1 : 0);
+    }
+    old = __shfl_sync(0xffffffffu, old, 0);
+    const unsigned long long ep = old / (unsigned long long)P + 1ull;
+    if (old % (unsigned long long)P == (unsigned long long)(P - 1)) {   // last arrival: release all
+      for (int cc = lane; cc < P; cc += 32)
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(bar + 16 * (1 + cc)), "l"(ep) : "memory");
+    }
+    if (lane == 0) {
+      const unsigned long long *flag = bar + 16 * (1 + blockIdx.x);
+      const unsigned long long t0 = globaltimer();
+      unsigned long long cur;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(flag) : "memory");
+        if (cur >= ep) break;
+        __nanosleep(32);
+        if (globaltimer() - t0 > 4000000000ull) __trap();
+      }
+      if (dbg) dbg[2] = clock64() - c0;
+      if (dbg) dbg[3] = clock64() - c0;
+    }
   }
+  consumers_sync();
 }
 
 // Transpose reduction of NV per-lane partials (NV a power of two <= 32): afterwards every
@@ -293,12 +283,8 @@ struct P2Ctx {
   int NS, SB, st_p1, st_p2, w0, w1, m, r, words, words_p2, zst;
   uint32_t ring0;
   float t;
-  const unsigned long long *g64;   // tagged g [B][r]
-  unsigned long long *mask64, *uni64;
-  uint32_t *mask_out;              // plain per-token words for the ABI (single layer) or NULL
-  uint32_t tag;
-  const unsigned long long *ctr;   // readiness counter of g
-  unsigned long long target;
+  const float *g;
+  uint32_t *mask, *uni;
 };
 
 template <typename T, int B, int CG>
@@ -309,37 +295,10 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   const int rchunks = x.r >> 3;
   long long tg0 = 0;
   if (x.trace && tid == 0) tg0 = clock64();
-  // g is read by every warp of every CTA: warp 0 fetches it once per CTA (polling the tags
-  // until every P1 row of this layer has been published), then it is broadcast via smem
-  if (warp == 0) {
-    if (lane == 0) ctr_wait(x.ctr, x.target);
-    __syncwarp();
-    const unsigned long long t0 = globaltimer();
-    const int nv = B * x.r;
-    for (int base = 0; base < nv; base += 32 * 16) {
-      bool done[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) done[k] = base + lane + 32 * k >= nv;
-      while (true) {
-        bool all = true;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          if (!done[k]) {
-            const int i = base + lane + 32 * k;
-            const unsigned long long v = ld_tagged(x.g64 + i);
-            if (tag_ok(v, x.tag)) {
-              x.sg[i] = tag_f(v);
-              done[k] = true;
-            } else {
-              all = false;
-            }
-          }
-        }
-        if (__all_sync(0xffffffffu, all)) break;
-        poll_pause(t0);
-      }
-    }
-  }
+  // g is read by every warp of every CTA: fetch it once per CTA (a 148-way instead of a
+  // 2368-way hot spot on the same L2 lines), then broadcast through shared memory
+  for (int i = tid * 4; i < B * x.r; i += kConsumers * 4)
+    *reinterpret_cast<float4 *>(x.sg + i) = __ldcg(reinterpret_cast<const float4 *>(x.g + i));
   consumers_sync();
   float gr[CG][8][B];
 #pragma unroll
@@ -414,13 +373,10 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       const float z = valid ? x.zbuf[b * x.zst + rl] + x.s_b2[rl] : __int_as_float(0x7fc00000);
       const uint32_t bits = __ballot_sync(0xffffffffu, z > x.t);
       u |= bits;
-      if (lane == 0) {
-        st_tagged(x.mask64 + (size_t)b * x.words + x.w0 + wl, tagged(x.tag, bits));
-        if (x.mask_out) x.mask_out[(size_t)b * x.words + x.w0 + wl] = bits;
-      }
+      if (lane == 0) x.mask[(size_t)b * x.words + x.w0 + wl] = bits;
     }
     if (lane == 0) {
-      st_tagged(x.uni64 + x.w0 + wl, tagged(x.tag, u));
+      x.uni[x.w0 + wl] = u;
       my_count += __popc(u);
     }
   }
@@ -461,8 +417,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
-  __shared__ uint32_t s_ep;
-  __shared__ unsigned long long s_seq;
   unsigned long long *trace = p.trace ? p.trace + (size_t)c * 256 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
 
@@ -485,16 +439,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     }
     mbar_init(ids_ready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    unsigned int e;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(p.epoch) : "memory");
-    s_ep = e;
-    s_seq = ld_tagged(p.ctr + 64);
   }
   __syncthreads();
-  const uint32_t ep = s_ep;
-  const unsigned long long seq = s_seq;
-  auto target = [&](int l) -> unsigned long long { return (seq + (unsigned long long)l + 1ull) * (unsigned long long)P; };
-  auto tag_of = [&](int l) -> uint32_t { return ep * 4096u + (uint32_t)l + 1u; };
 
   // =====================================================================================
   // producer warp: streams layer after layer; runs ahead into the next layer's P1 and P2
@@ -561,7 +507,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 
   for (int l = 0; l < L; ++l) {
     const LayerW lw = layer(l);
-    const uint32_t tag = tag_of(l);
+    const float *xin = (l == 0) ? p.x : p.xbuf;
+    float *yout = (l == L - 1) ? p.y : p.xbuf;
     unsigned long long *tr = (l == (L > 1 ? 1 : 0)) ? trace : nullptr;   // steady-state layer
     const uint32_t ring0 = ring;
     auto wait_full = [&](uint32_t it) {
@@ -574,51 +521,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
     float sc[B];
     if (is_up) {
-      if (l == 0) {
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
+      for (int q = 0; q < CH; ++q) {
+        const int ch = gt + q * kGroup;
 #pragma unroll
-          for (int b = 0; b < B; ++b) {
-            if (ch < chunks) {
-              const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(p.x + (size_t)b * d + ch * 8));
-              const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(p.x + (size_t)b * d + ch * 8) + 1);
-              xr[q][0][b] = a0.x; xr[q][1][b] = a0.y; xr[q][2][b] = a0.z; xr[q][3][b] = a0.w;
-              xr[q][4][b] = a1.x; xr[q][5][b] = a1.y; xr[q][6][b] = a1.z; xr[q][7][b] = a1.w;
-            } else {
+        for (int b = 0; b < B; ++b) {
+          if (ch < chunks) {
+            const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8));
+            const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8) + 1);
+            xr[q][0][b] = a0.x; xr[q][1][b] = a0.y; xr[q][2][b] = a0.z; xr[q][3][b] = a0.w;
+            xr[q][4][b] = a1.x; xr[q][5][b] = a1.y; xr[q][6][b] = a1.z; xr[q][7][b] = a1.w;
+          } else {
 #pragma unroll
-              for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
-            }
-          }
-        }
-      } else {
-        // x_l = y_{l-1}: wait for every CTA's reduction of layer l-1, then read the tagged words
-        if (gt == 0) ctr_wait(p.ctr + 48, target(l - 1));
-        up_sync();
-        const uint32_t tprev = tag_of(l - 1);
-        const unsigned long long t0 = globaltimer();
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            if (ch < chunks) {
-              const unsigned long long *src = p.x64 + (size_t)b * d + ch * 8;
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) {
-                unsigned long long v0, v1;
-                while (true) {
-                  ld_tagged2(src + e, v0, v1);
-                  if (tag_ok(v0, tprev) && tag_ok(v1, tprev)) break;
-                  poll_pause(t0);
-                }
-                xr[q][e][b] = tag_f(v0);
-                xr[q][e + 1][b] = tag_f(v1);
-              }
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
-            }
+            for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
           }
         }
       }
@@ -683,20 +598,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           const int j = c + (k0 + k) * P;
           float u = up_total(rb, gt) * sc[b] + s_b1[k0 + k];
           if (p.pred_relu) u = fmaxf(u, 0.f);
-          st_tagged(p.g64 + (size_t)b * r + j, tagged(tag, __float_as_uint(u)));
+          p.g[(size_t)b * r + j] = u;
         }
       }
     }
-    if (is_up) {
-      up_sync();                       // every up thread has issued its g stores
-      if (gt == 0) ctr_add(p.ctr + 0);
-    }
     if (tr && tid == 0) tr[1] = globaltimer();
+    grid_sync(p.bar, P, tr ? tr + 204 : nullptr);
+    if (tr && tid == 0) tr[2] = globaltimer();
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
       P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, sg, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
-                r, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g64, p.mask64, p.uni64, p.mask_out, tag, p.ctr + 0, target(l)};
+                r, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
       const int cg = ((r >> 3) + 31) / 32;
       if (cg <= 1) p2_phase<T, B, 1>(ctx);
       else if (cg == 2) p2_phase<T, B, 2>(ctx);
@@ -704,33 +617,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       else p2_phase<T, B, 4>(ctx);
     }
     consumers_sync();
-    if (tid == 0) {
-      st_tagged(p.cnt64 + c, tagged(tag, (uint32_t)s_count));   // (mask and union words were issued before
-      ctr_add(p.ctr + 16);                                        //  the consumers_sync above)
-    }
-    if (tr && tid == 0) tr[2] = globaltimer();
+    if (tid == 0) p.counts[c] = s_count;
+    grid_sync(p.bar, P);
+    if (tr && tid == 0) tr[4] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
     if (warp == 0) {
       // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
       constexpr int KPL = 8;  // counts per lane (P <= 256)
       int cv[KPL];
-      if (lane == 0) ctr_wait(p.ctr + 16, target(l));
-      __syncwarp();
-      {
-        const unsigned long long t0 = globaltimer();
 #pragma unroll
-        for (int i = 0; i < KPL; ++i) {
-          const int b = lane * KPL + i;
-          cv[i] = 0;
-          if (b < P) {
-            unsigned long long v;
-            while (!tag_ok(v = ld_tagged(p.cnt64 + b), tag)) poll_pause(t0);
-            cv[i] = (int)(uint32_t)v;
-          }
-        }
+      for (int i = 0; i < KPL; ++i) {
+        const int b = lane * KPL + i;
+        cv[i] = (b < P) ? __ldcg(p.counts + b) : 0;
       }
-      if (tr && lane == 0) tr[4] = globaltimer();
       int lsum = 0;
 #pragma unroll
       for (int i = 0; i < KPL; ++i) lsum += cv[i];
@@ -760,23 +660,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         int w = (int)(((int64_t)blk * p.words) / P);
         while (before < k1 && w < p.words) {
           const int ww = w + lane;
-          const unsigned long long t0 = globaltimer();
-          uint32_t u = 0u;
-          if (ww < p.words) {
-            unsigned long long v;
-            while (!tag_ok(v = ld_tagged(p.uni64 + ww), tag)) poll_pause(t0);
-            u = (uint32_t)v;
-          }
+          const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
           uint32_t bitsb[B];
 #pragma unroll
-          for (int b = 0; b < B; ++b) {
-            bitsb[b] = u;
-            if (B > 1 && ww < p.words) {
-              unsigned long long v;
-              while (!tag_ok(v = ld_tagged(p.mask64 + (size_t)b * p.words + ww), tag)) poll_pause(t0);
-              bitsb[b] = (uint32_t)v;
-            }
-          }
+          for (int b = 0; b < B; ++b)
+            bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
           const int cnt = __popc(u);
           int wincl = cnt;
 #pragma unroll
@@ -919,23 +807,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         if (ch < chunks) {
 #pragma unroll
           for (int b = 0; b < B; ++b) {
-            unsigned long long *dst = p.yp64 + ((size_t)c * B + b) * d + ch * 8;
-#pragma unroll
-            for (int e = 0; e < 8; e += 2)
-              st_tagged2(dst + e, tagged(tag, __float_as_uint(yr[q][e][b])), tagged(tag, __float_as_uint(yr[q][e + 1][b])));
+            float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
+            __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
+            __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
           }
         }
       }
     }
     ring = it_ffn + n_st;
 
-    consumers_sync();                  // every down thread has issued its partial stores
-    if (tid == 0) {
-      ctr_add(p.ctr + 32);
-      ctr_wait(p.ctr + 32, target(l));
-    }
-    consumers_sync();
     if (tr && tid == 0) tr[6] = globaltimer();
+    grid_sync(p.bar, P, tr ? tr + 208 : nullptr);
+    if (tr && tid == 0) tr[7] = globaltimer();
 
     // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
     {
@@ -950,29 +833,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         const int b = it2 / ncol, j = j0 + it2 % ncol;
         const int c0 = (sgp * P) / SPL, c1 = ((sgp + 1) * P) / SPL;
         float v[PPG];
-        const unsigned long long t0 = globaltimer();
-        bool ok[PPG];
 #pragma unroll
-        for (int q = 0; q < PPG; ++q) ok[q] = c0 + q >= c1;
-        while (true) {
-          bool all = true;
-#pragma unroll
-          for (int q = 0; q < PPG; ++q) {
-            if (!ok[q]) {
-              const unsigned long long w = ld_tagged(p.yp64 + ((size_t)(c0 + q) * B + b) * d + j);
-              if (tag_ok(w, tag)) {
-                v[q] = tag_f(w);
-                ok[q] = true;
-              } else {
-                all = false;
-              }
-            } else if (c0 + q >= c1) {
-              v[q] = 0.f;
-            }
-          }
-          if (all) break;
-          poll_pause(t0);
-        }
+        for (int q = 0; q < PPG; ++q) v[q] = (c0 + q < c1) ? __ldcg(p.ypart + ((size_t)(c0 + q) * B + b) * d + j) : 0.f;
         float acc = 0.f;
 #pragma unroll
         for (int q = 0; q < PPG; ++q) acc += v[q];
@@ -985,17 +847,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 #pragma unroll
         for (int sgp = 0; sgp < SPL; ++sgp) acc += part[sgp * items + it2];
         if (lw.b_down) acc += WT<T>::to_float(lw.b_down, j);
-        if (l == L - 1) p.y[(size_t)b * d + j] = acc;
-        else st_tagged(p.x64 + (size_t)b * d + j, tagged(tag, __float_as_uint(acc)));
+        yout[(size_t)b * d + j] = acc;
       }
     }
-    consumers_sync();   // every x store of this CTA issued; smem of this layer is free
-    if (tid == 0) ctr_add(p.ctr + 48);   // every layer, so the counter stays at (seq + l + 1) P
     if (tr && tid == 0) tr[8] = globaltimer();
-  }
-  if (c == 0 && tid == 0) {   // every CTA read the epoch and the layer sequence long ago
-    atomicAdd(p.epoch, 1u);
-    st_tagged(p.ctr + 64, seq + (unsigned long long)L);
+    if (l < L - 1) grid_sync(p.bar, P);   // the next layer reads all of y
   }
 }
 
@@ -1034,34 +890,20 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.pcap = (d + w.P - 1) / w.P + 1;
   w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * r * 4 + 64;
   const int words = (m + 31) / 32;
-  const int mb = kFusedMaxB;
-  (void)maxB;
-  if (!alloc((void **)&w.epoch, 64)) return false;
-  if (!alloc((void **)&w.ctr, 80 * 8)) return false;
-  if (!alloc((void **)&w.g64, (size_t)mb * r * 8)) return false;
-  if (!alloc((void **)&w.yp64, (size_t)w.P * mb * d * 8)) return false;
-  if (!alloc((void **)&w.cnt64, (size_t)w.P * 8)) return false;
-  if (!alloc((void **)&w.mask64, (size_t)mb * words * 8)) return false;
-  if (!alloc((void **)&w.uni64, (size_t)words * 8)) return false;
-  if (!alloc((void **)&w.x64, (size_t)mb * d * 8)) return false;
-  w.ws_bytes = (size_t)mb * r * 8 + (size_t)w.P * mb * d * 8 + (size_t)w.P * 8 + (size_t)mb * words * 8 +
-               (size_t)words * 8 + (size_t)mb * d * 8;
+  if (!alloc((void **)&w.bar, (size_t)(1 + num_sms) * 128 + 128)) return false;
+  if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
+  if (!alloc((void **)&w.ypart, (size_t)w.P * std::min(maxB, kFusedMaxB) * d * 4)) return false;
+  if (!alloc((void **)&w.counts, (size_t)w.P * 4)) return false;
+  if (!alloc((void **)&w.mask, (size_t)maxB * words * 4)) return false;
+  if (!alloc((void **)&w.uni, (size_t)words * 4)) return false;
+  if (!alloc((void **)&w.xbuf, (size_t)std::min(maxB, kFusedMaxB) * d * 4)) return false;
   if (w.smem > 227 * 1024) return true;
   w.enabled = true;
   return true;
 }
 
 inline void fused_init(FusedWork &w, cudaStream_t s) {
-  if (!w.enabled) return;   // tag 0 is never current: zeroed buffers read as "not yet published"
-  cudaMemsetAsync(w.epoch, 0, 64, s);
-  cudaMemsetAsync(w.ctr, 0, 80 * 8, s);
-  const int mb = kFusedMaxB, words = (w.m + 31) / 32;
-  cudaMemsetAsync(w.g64, 0, (size_t)mb * w.r * 8, s);
-  cudaMemsetAsync(w.yp64, 0, (size_t)w.P * mb * w.d * 8, s);
-  cudaMemsetAsync(w.cnt64, 0, (size_t)w.P * 8, s);
-  cudaMemsetAsync(w.mask64, 0, (size_t)mb * words * 8, s);
-  cudaMemsetAsync(w.uni64, 0, (size_t)words * 8, s);
-  cudaMemsetAsync(w.x64, 0, (size_t)mb * w.d * 8, s);
+  if (w.enabled) cudaMemsetAsync(w.bar, 0, (size_t)(1 + w.P) * 128 + 128, s);
 }
 
 // neurons per stage (NA template bound and runtime G) and P1 rows per stage
@@ -1119,7 +961,7 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.L = 1;
   p.x = a.x;
   p.y = a.y;
-  p.x64 = w.x64;
+  p.xbuf = w.xbuf;
   p.d = a.d;
   p.m = a.m;
   p.r = a.r;
@@ -1127,16 +969,14 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.B = a.B;
   p.rmsnorm = a.rmsnorm;
   p.pred_relu = a.pred_relu;
-  p.mask_out = a.mask_out;
+  p.mask = a.mask_out ? a.mask_out : w.mask;
+  p.uni = w.uni;
   p.ids_out = a.ids_out;
   p.n_out = a.n_out;
-  p.g64 = w.g64;
-  p.mask64 = w.mask64;
-  p.uni64 = w.uni64;
-  p.cnt64 = w.cnt64;
-  p.yp64 = w.yp64;
-  p.epoch = w.epoch;
-  p.ctr = w.ctr;
+  p.g = w.g;
+  p.ypart = w.ypart;
+  p.counts = w.counts;
+  p.bar = w.bar;
   p.NS = w.NS;
   p.stage_bytes = w.stage_bytes;
   p.words_p2 = w.words_p2;
@@ -1181,7 +1021,7 @@ inline cudaError_t fused_launch_stack(FusedWork &w, const FusedArgs &a, const La
   FusedParams p = fused_params(w, a);
   p.lws = lws;
   p.L = L;
-  p.mask_out = nullptr;
+  p.mask = w.mask;
   p.ids_out = nullptr;
   return fused_launch_p<T>(w, p, a.reglu, a.B, s);
 }

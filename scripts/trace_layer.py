@@ -16,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2312_12456_b200 import gen, pi  # noqa: E402
 from paper_2312_12456_b200.stack import algorithmic_bytes, build_stack  # noqa: E402
 
-NAMES = ["start", "P1 done", "counts published", "P2 done", "counts received", "ids ready", "FFN done", "unused", "end"]
+NAMES = ["start", "P1 done", "grid bar 1", "P2 done", "grid bar 2", "ids ready", "FFN done", "grid bar 3", "end"]
 
 
 def main():
