@@ -331,9 +331,18 @@ def main():
     kname = ("k_layer x%d layers in one persistent launch (pi_stack_run)" % n_layers) if world == 1 and \
         launches_per_layer == 1 else "pi_layer_forward (%d launch(es) per layer)" % launches_per_layer
     launches_per_step = 1 if (world == 1 and launches_per_layer == 1) else n_layers * launches_per_layer
+    traffic, traffic_src = None, None
+    try:   # DRAM bytes / algorithmic bytes from the committed ncu --set full capture of this kernel
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if world == 1 and args.config == "c4":
+            traffic = int(tj["ratio"] * bytes_launch)
+            traffic_src = "%s (ratio %.3f of algorithmic bytes, scaled to this launch)" % (tj["capture"], tj["ratio"])
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": None, "peak_source": peak_src,
+                "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "bytes_per_launch": int(bytes_launch), "launch_us": round(launch_s * 1e6, 2),
                 "step_frac": round(float(bytes_step.sum(axis=1).mean()) / (ms_per_step / 1e3) / 1e9 / peak, 4)}
 
