@@ -143,6 +143,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
 }
+// L2 prefetch of a global range (no shared memory, fire and forget), kept with evict_last
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src), "r"(bytes), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -213,7 +223,7 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsign
         if (globaltimer() - t0 > 4000000000ull) __trap();
       }
       if (dbg) dbg[2] = clock64() - c0;
-      if (dbg) dbg[3] = clock64() - c0;
+      if (dbg) dbg[3] = globaltimer();
     }
   }
   consumers_sync();
@@ -289,7 +299,7 @@ struct P2Ctx {
 
 template <typename T, int B, int CG>
 __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
-  constexpr int RR = (B == 1) ? 2 : 1;   // rows per warp per iteration
+  constexpr int RR = (B == 1) ? 4 : 2;   // rows per warp per iteration
   constexpr int NV = Pow2Ceil<RR * B>::v;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rchunks = x.r >> 3;
@@ -323,7 +333,9 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     for (int q = 0; q < CG; ++q) sgr += gr[q][0][0];
     x.trace[200] = (unsigned long long)(clock64() - tg0) + (sgr == 1.2345f ? 1 : 0);
   }
-  for (int st = 0; st < x.st_p2; ++st) {
+  // the two warp groups (warps 0-7, 8-15) take alternate stages, so two stages are in flight
+  const int grp = warp >> 3, gw8 = warp & 7;
+  for (int st = grp; st < x.st_p2; st += 2) {
     const uint32_t it = x.st_p1 + st;
     const int wa = x.w0 + st * x.words_p2, wb = min(x.w1, wa + x.words_p2);
     const int nrows = min(x.m, wb * 32) - wa * 32;
@@ -331,7 +343,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
     if (x.trace && tid == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
     const uint8_t *buf = x.stages + (size_t)(it % x.NS) * x.SB;
-    for (int rb0 = warp * RR; rb0 < nrows; rb0 += kConsumerWarps * RR) {
+    for (int rb0 = gw8 * RR; rb0 < nrows; rb0 += kGroupWarps * RR) {
       float v[NV];
 #pragma unroll
       for (int i = 0; i < NV; ++i) v[i] = 0.f;
@@ -357,9 +369,9 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       const float z = warp_reduce_multi<NV>(v);   // lane l: token (l / RR) % B, row l % RR
       if (lane < RR * B) x.zbuf[(lane / RR) * x.zst + zoff + rb0 + (lane % RR)] = z;
     }
-    if (tid == 0) mbar_arrive(&x.hready[it % x.NS]);   // keep hready phases = ring uses
+    if (gw8 == 0 && lane == 0) mbar_arrive(&x.hready[it % x.NS]);   // keep hready phases = ring uses
     __syncwarp();
-    if (lane == 0) mbar_arrive(&x.empty[it % x.NS]);   // this warp is done with the stage
+    if (lane == 0) mbar_arrive_cnt(&x.empty[it % x.NS], 2);   // 8 warps of this group x 2
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
   // ballots: one warp per mask word -> per-token words, union word, popcount
@@ -477,6 +489,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
         uint8_t *dst = acquire(bytes);
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
+      }
+      if (l + 1 < L) {
+        // while this layer synchronises and compacts (little HBM traffic), pull the next
+        // layer's predictor rows for this CTA into L2; its ring loads then hit L2
+        const LayerW nx = layer(l + 1);
+        const uint64_t keep = policy_evict_last();
+        for (int k = 0; k < n_p1; ++k)
+          prefetch_l2(nx.p_w1 + (size_t)(c + k * P) * row_dn, (uint32_t)row_dn, keep);
+        const size_t a0 = (size_t)w0 * 32 * rowb2, a1 = (size_t)min(m, w1 * 32) * rowb2;
+        for (size_t o = a0; o < a1; o += 32768)
+          prefetch_l2(nx.p_w2 + o, (uint32_t)min((size_t)32768, a1 - o), keep);
       }
       mbar_wait(ids_ready, l & 1);                 // phase 3: after the ids are published
       const int n_mine = s_k1 - s_k0;
@@ -618,7 +641,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     }
     consumers_sync();
     if (tid == 0) p.counts[c] = s_count;
-    grid_sync(p.bar, P);
+    grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
     if (tr && tid == 0) tr[4] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
@@ -851,7 +874,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
     }
     if (tr && tid == 0) tr[8] = globaltimer();
-    if (l < L - 1) grid_sync(p.bar, P);   // the next layer reads all of y
+    if (l < L - 1) grid_sync(p.bar, P, tr ? tr + 216 : nullptr);   // the next layer reads all of y
   }
 }
 

@@ -60,7 +60,7 @@ def main():
         issue = np.where(full[:, 72:128] > 0, (full[:, 72:128] - t0) / 1e3, np.nan)
         stage_rows.append((ready, issue))
         gl = full[:, 200]
-        b1 = full[:, 204:208]; b3 = full[:, 208:212]
+        bars = [full[:, 204 + 4 * k:208 + 4 * k].copy() for k in range(4)]
         raw = full[:, 128:192].reshape(P, 16, 4)
         base = raw[:, 0, 3:4]
         dbg = np.where(raw > 0, raw - base[:, :, None] if False else raw - raw[:, :1, 3:4], np.nan)
@@ -74,8 +74,11 @@ def main():
            "phases_us_max_over_ctas": dict(zip(NAMES, np.round(mx, 2).tolist())),
            "ideal_us_at_peak": round(nb / 6560.6e9 * 1e6, 2)}
     out["g_load_cycles_median_max"] = [float(np.median(gl)), float(gl.max())]
-    out["bar1_cycles_fence_atom_flag_fence_median"] = np.median(b1, axis=0).tolist()
-    out["bar3_cycles_fence_atom_flag_fence_median"] = np.median(b3, axis=0).tolist()
+    for k, nm in enumerate(["B1", "B3", "B2", "B4"]):
+        bk = bars[k]
+        rel_done = (bk[:, 3] - t0) / 1e3
+        out[nm + "_cycles_atomret_flagseen_median"] = [float(np.median(bk[:, 1])), float(np.median(bk[:, 2]))]
+        out[nm + "_release_us_min_max"] = [float(rel_done.min()), float(rel_done.max())]
     rd, iss = stage_rows[-1]
     for cta in (0, P // 2):
         k = int(np.sum(~np.isnan(rd[cta])))
