@@ -95,6 +95,13 @@ typedef struct {
                             reading R3); -INFINITY => all finite logits; NaN logits inactive */
   int32_t max_batch;     /* 1..PI_MAX_BATCH; sizes the workspace                               */
   uint32_t flags;        /* PI_FLAG_*                                                          */
+  /* Hot neurons (Insight-1): the profiler's activation frequency f_i (Eq. 1,
+   * P:680-690) of the GLOBAL layer, host [m_total], or NULL.  Neurons of this shard with
+   * f_i >= hot_freq are "hot": while the layer runs its predictor and synchronises, the fused
+   * kernel pulls their up/down rows into L2 so the FFN phase streams them from L2 instead of
+   * HBM.  Results are unchanged (hotness only affects data movement). */
+  const float *neuron_freq;
+  float hot_freq;
 } pi_layer_desc;
 
 typedef struct {

@@ -75,13 +75,16 @@ struct FusedArgs {
   bool rmsnorm, pred_relu, reglu;
   uint32_t *mask_out;
   int32_t *ids_out, *n_out;
+  const int32_t *hot_ids;
+  int n_hot;
 };
 
 struct LayerW {  // one layer's library-owned weights (device pointers)
   const uint8_t *w_up, *w_down, *p_w1, *p_w2;
   const void *b_up, *b_down, *p_b1, *p_b2;
+  const int32_t *hot_ids;   // local ids of the hot neurons (L2-prefetched each step), or NULL
+  int n_hot;
   float t;
-  int pad;
 };
 
 struct FusedParams {
@@ -100,6 +103,7 @@ struct FusedParams {
   unsigned long long *bar;
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
+  int knobs;                  // experiment switches (PI_FUSED_KNOBS); 0 = production behaviour
 };
 
 // ---------------------------------------------------------------------------
@@ -490,7 +494,18 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         uint8_t *dst = acquire(bytes);
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
       }
-      if (l + 1 < L) {
+      if (lw.n_hot) {
+        // hot neurons (activation frequency >= hot_freq) are almost surely active: pull this
+        // CTA's share of their up/down rows into L2 now, while the layer runs its predictor and
+        // synchronises; the FFN phase then streams them from L2
+        const uint64_t keep = policy_evict_last();
+        for (int k = c; k < lw.n_hot; k += P) {
+          const int i = lw.hot_ids[k];
+          prefetch_l2(lw.w_up + (size_t)i * row_up, (uint32_t)row_up, keep);
+          prefetch_l2(lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, keep);
+        }
+      }
+      if (l + 1 < L && (p.knobs & 1)) {   // measured slower (2.533 vs 2.512 ms/step, c4): opt-in
         // while this layer synchronises and compacts (little HBM traffic), pull the next
         // layer's predictor rows for this CTA into L2; its ring loads then hit L2
         const LayerW nx = layer(l + 1);
@@ -980,6 +995,8 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.lw0.p_b1 = a.p_b1;
   p.lw0.p_b2 = a.p_b2;
   p.lw0.t = a.threshold;
+  p.lw0.hot_ids = a.hot_ids;
+  p.lw0.n_hot = a.n_hot;
   p.lws = nullptr;
   p.L = 1;
   p.x = a.x;
@@ -1008,6 +1025,10 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.part_off = w.part_off;
   p.pcap = w.pcap;
   p.trace = w.trace;
+  {
+    const char *e = getenv("PI_FUSED_KNOBS");
+    p.knobs = e ? atoi(e) : 0;
+  }
   return p;
 }
 

@@ -85,6 +85,8 @@ struct pi_layer {
   int32_t *n_active = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;  // [max_batch, d] each (stack ping-pong)
   float *hx = nullptr, *hy = nullptr;      // [max_batch, d] each (host-buffer entry points)
+  int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons
+  int n_hot = 0;
   FusedWork fw{};             // fused-kernel workspace
   int tiles = 0, S = 0;
   int64_t weight_bytes = 0, ws_bytes = 0;
@@ -268,6 +270,21 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
 #undef ALLOC
 
   cudaStream_t s = (cudaStream_t)stream;
+  if (D->neuron_freq) {
+    std::vector<int32_t> hot;
+    for (int k = 0; k < ml; ++k) {
+      const int gid = D->neuron_ids ? D->neuron_ids[k] : k;
+      const float f = D->neuron_freq[gid];
+      if (std::isfinite(f) && f >= D->hot_freq) hot.push_back(k);
+    }
+    if (!hot.empty()) {
+      st = dev_alloc(L, (void **)&L->hot_ids, hot.size() * 4, false);
+      if (st != PI_OK) return cleanup(st);
+      if (cudaMemcpy(L->hot_ids, hot.data(), hot.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        return cleanup(fail(PI_ERR_CUDA, "layer %d: hot table copy", lid));
+      L->n_hot = (int)hot.size();
+    }
+  }
   int32_t *d_nid = nullptr;
   if (D->neuron_ids) {
     if (cudaMalloc(&d_nid, (size_t)ml * 4) != cudaSuccess)
@@ -367,7 +384,8 @@ extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, 
     h[l].p_b1 = Ll->p_b1;
     h[l].p_b2 = Ll->p_b2;
     h[l].t = Ll->threshold;
-    h[l].pad = 0;
+    h[l].hot_ids = Ll->hot_ids;
+    h[l].n_hot = Ll->n_hot;
   }
   if (cudaMalloc(&S->lws, sizeof(LayerW) * n_layers) != cudaSuccess) {
     delete S;
@@ -579,6 +597,7 @@ static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint3
       a.threshold = L->threshold; a.rmsnorm = (L->flags & PI_FLAG_INPUT_RMSNORM) != 0;
       a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
       a.mask_out = mask_out; a.ids_out = ids_out; a.n_out = n_out;
+      a.hot_ids = L->hot_ids; a.n_hot = L->n_hot;
       cudaError_t e = fused_launch<T>(L->fw, a, L->num_sms, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "layer %d: fused launch: %s", L->layer_id, cudaGetErrorString(e));
       return PI_OK;

@@ -54,7 +54,8 @@ class LayerDesc(ctypes.Structure):
                 ("b_up", ctypes.c_void_p), ("b_down", ctypes.c_void_p), ("p_w1", ctypes.c_void_p),
                 ("p_b1", ctypes.c_void_p), ("p_w2", ctypes.c_void_p), ("p_b2", ctypes.c_void_p),
                 ("logit_threshold", ctypes.c_float), ("max_batch", ctypes.c_int32),
-                ("flags", ctypes.c_uint32)]
+                ("flags", ctypes.c_uint32), ("neuron_freq", ctypes.POINTER(ctypes.c_float)),
+                ("hot_freq", ctypes.c_float)]
 
 
 class LayerInfo(ctypes.Structure):
@@ -137,7 +138,7 @@ class Layer:
 
     def __init__(self, w, neuron_ids: Optional[Sequence[int]] = None, max_batch: int = 1, flags: int = 0,
                  layer_id: int = 0, threshold: Optional[float] = None, pred_act: Optional[str] = None,
-                 own_b_down: bool = True, stream=None):
+                 own_b_down: bool = True, stream=None, neuron_freq=None, hot_freq: float = 0.9):
         self.handle = None
         dt = w.w_up.dtype
         if dt not in _DT:
@@ -151,13 +152,18 @@ class Layer:
             ids = self._ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
             m_local = len(self._ids)
         thr = w.threshold if threshold is None else threshold
+        freq_p = None
+        if neuron_freq is not None:
+            self._freq = np.ascontiguousarray(np.asarray(neuron_freq, dtype=np.float32))
+            assert self._freq.shape[0] == m_total
+            freq_p = self._freq.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         pa = (pred_act or getattr(w, "pred_act", "relu"))
         desc = LayerDesc(layer_id, d, m_total, r, m_local, ids, _DT[dt],
                          PI_ACT_REGLU if w.act == "reglu" else PI_ACT_RELU,
                          PI_PRED_RELU if pa == "relu" else PI_PRED_LINEAR,
                          _ptr(w.w_up), _ptr(w.w_gate), _ptr(w.w_down), _ptr(w.b_up),
                          _ptr(w.b_down) if own_b_down else None, _ptr(w.p_w1), _ptr(w.p_b1), _ptr(w.p_w2),
-                         _ptr(w.p_b2), float(thr), int(max_batch), int(flags))
+                         _ptr(w.p_b2), float(thr), int(max_batch), int(flags), freq_p, float(hot_freq))
         h = ctypes.c_void_p()
         s = _stream(stream)
         _check(_lib.pi_layer_create(ctypes.byref(desc), s, ctypes.byref(h)))

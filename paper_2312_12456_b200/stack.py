@@ -88,7 +88,7 @@ def shard_ids(p: np.ndarray, world: int, rank: int, granule: int = 64) -> Option
 
 def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, world: int = 1, seed: int = 0,
                 device="cuda", max_batch: int = 1, mean_act: float = 0.10, group=None,
-                keep_weights: bool = False, dims: Optional[dict] = None):
+                keep_weights: bool = False, dims: Optional[dict] = None, hot_freq: Optional[float] = None):
     """Generate the config's layers (random init, seeded) and create this rank's handles.
 
     Returns (Stack, weights-or-None).  With keep_weights the generator tensors stay alive
@@ -102,7 +102,10 @@ def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, 
         w = gen.make_layer(cfg, layer=l, seed=seed, device=device, mean_act=mean_act, **dims)
         nid = shard_ids(w.p, world, rank)
         own = rank == 0
-        layers.append(pi.Layer(w, neuron_ids=nid, max_batch=max_batch, flags=flags, layer_id=l, own_b_down=own))
+        # the planted activity profile plays the paper's profiler frequencies f_i (Eq. 1)
+        freq = None if hot_freq is None else w.p
+        layers.append(pi.Layer(w, neuron_ids=nid, max_batch=max_batch, flags=flags, layer_id=l, own_b_down=own,
+                               neuron_freq=freq, hot_freq=hot_freq if hot_freq is not None else 2.0))
         m_local = w.m if nid is None else len(nid)
         metas.append(LayerMeta(w.d, m_local, w.r, w.act == "reglu", w.b_up is not None,
                                own and w.b_down is not None, w.p_b1 is not None, w.p_b2 is not None))
