@@ -474,10 +474,32 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
     };
+    const size_t rowb2 = (size_t)r * 2;
     for (int l = 0; l < L; ++l) {
       const LayerW lw = layer(l);
       if (l == (L > 1 ? 1 : 0)) trace_it0 = it;
+      // The ring holds the layer's first NS predictor stages (issued while the previous layer
+      // finished its FFN); stages >= NS can only be issued once the consumers free slots after
+      // grid barrier 1, i.e. on the critical path.  When stage NS is next -- the previous
+      // layer's FFN has been fully consumed, and HBM idles through its reduction and the
+      // barriers -- pull those stages' rows into L2 so their ring loads hit L2.
+      auto prefetch_tail = [&](int li) {
+        if (li != NS || (p.knobs & 2)) return;
+        const uint64_t keep = policy_evict_last();
+        for (int st = NS; st < st_p1; ++st) {
+          const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
+          for (int k = 0; k < kn; ++k)
+            prefetch_l2(lw.p_w1 + (size_t)(c + (k0 + k) * P) * row_dn, (uint32_t)row_dn, keep);
+        }
+        const int s2 = max(0, NS - st_p1);
+        if (s2 < st_p2) {
+          const size_t a0 = (size_t)(w0 + s2 * p.words_p2) * 32 * rowb2, a1 = (size_t)min(m, w1 * 32) * rowb2;
+          for (size_t o = a0; o < a1; o += 32768)
+            prefetch_l2(lw.p_w2 + o, (uint32_t)min((size_t)32768, a1 - o), keep);
+        }
+      };
       for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
+        prefetch_tail(st);
         const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
         uint8_t *dst = acquire((uint32_t)(kn * row_dn));
         const int s = it % NS;
@@ -486,8 +508,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           bulk_g2s(dst + (size_t)k * row_dn, lw.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
         }
       }
-      const size_t rowb2 = (size_t)r * 2;
       for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 rows of words [w0, w1), contiguous
+        prefetch_tail(st_p1 + st);
         const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
         const int ra = wa * 32, rb = min(m, wb * 32);
         const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
@@ -660,14 +682,29 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     if (tr && tid == 0) tr[4] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
+    // One L2 round trip: all consumer threads stage the P counts, the union words and (B > 1)
+    // the per-token words into the ring slot the first FFN stage will use -- free now: every
+    // predictor stage has been consumed and the producer waits for ids_ready before reusing it.
+    const uint32_t it_ffn = ring + st_p1 + st_p2;
+    uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
+    uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (B > 1)
+    int *c_cnt = reinterpret_cast<int *>(c_msk + (B > 1 ? B * p.words : 0));   // [P]
+    for (int i = tid; i < p.words; i += kConsumers) {
+      c_uni[i] = __ldcg(p.uni + i);
+      if (B > 1)
+#pragma unroll
+        for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
+    }
+    if (tid < P) c_cnt[tid] = __ldcg(p.counts + tid);
+    consumers_sync();
     if (warp == 0) {
-      // the P per-CTA counts in one round trip (CTA-block b owns words [b W/P, (b+1) W/P))
+      // CTA-block b owns words [b W/P, (b+1) W/P)
       constexpr int KPL = 8;  // counts per lane (P <= 256)
       int cv[KPL];
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int b = lane * KPL + i;
-        cv[i] = (b < P) ? __ldcg(p.counts + b) : 0;
+        cv[i] = (b < P) ? c_cnt[b] : 0;
       }
       int lsum = 0;
 #pragma unroll
@@ -698,11 +735,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         int w = (int)(((int64_t)blk * p.words) / P);
         while (before < k1 && w < p.words) {
           const int ww = w + lane;
-          const uint32_t u = (ww < p.words) ? __ldcg(p.uni + ww) : 0u;
+          const uint32_t u = (ww < p.words) ? c_uni[ww] : 0u;
           uint32_t bitsb[B];
 #pragma unroll
-          for (int b = 0; b < B; ++b)
-            bitsb[b] = (B > 1 && ww < p.words) ? __ldcg(p.mask + (size_t)b * p.words + ww) : u;
+          for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? c_msk[b * p.words + ww] : u;
           const int cnt = __popc(u);
           int wincl = cnt;
 #pragma unroll
@@ -735,6 +771,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         s_k1 = k1;
       }
     }
+    // generic-proxy writes to the scratch slot before the producer's TMA overwrites it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     consumers_sync();
     if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
     if (tr && tid == 0) tr[5] = globaltimer();
@@ -748,7 +786,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     consumers_sync();
 
     // ---------------- phase 3: the sparse FFN ----------------
-    const uint32_t it_ffn = ring + st_p1 + st_p2;
     const int n_st = (n_mine + G - 1) / G;
     if (is_up) {
       constexpr int NV = NA * B * (REGLU ? 2 : 1);
@@ -917,6 +954,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.NS = (int)(budget / sb);
   if (w.NS < 2) return true;
   w.stage_bytes = (int)sb;
+  // compaction stages the union words, the per-token words and the P counts in one ring slot
+  if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)num_sms * 4 > sb) return true;
   w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / ((size_t)32 * r * 2)));
   w.idcap = (m + w.P - 1) / w.P + 2;
   const int words_all = (m + 31) / 32;
