@@ -199,7 +199,8 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // the episode writes e into every CTA's flag (warp 0 of that CTA, 32 lanes in parallel), and
 // every CTA polls only its own flag -- no L2 line is polled by 148 SMs at once, so the
 // arrivals are not slowed by the pollers.  A 4-second watchdog traps instead of hanging.
-__device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsigned long long *dbg = nullptr) {
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsigned long long *dbg = nullptr,
+                                          bool flags = false) {
   consumers_sync();  // every consumer thread of this CTA has issued its global writes
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -212,6 +213,24 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsign
     }
     old = __shfl_sync(0xffffffffu, old, 0);
     const unsigned long long ep = old / (unsigned long long)P + 1ull;
+    if (!flags) {
+      // every CTA polls the counter itself: one round trip fewer than a flag release by the
+      // last arrival (scripts/microbench_barrier.cu: 1.39 vs 1.87 us per barrier, idle GPU)
+      if (lane == 0) {
+        const unsigned long long t0 = globaltimer(), target = ep * (unsigned long long)P;
+        while (true) {
+          unsigned long long cur;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+          if (cur >= target) break;
+          __nanosleep(32);
+          if (globaltimer() - t0 > 4000000000ull) __trap();
+        }
+        if (dbg) dbg[2] = clock64() - c0;
+        if (dbg) dbg[3] = globaltimer();
+      }
+      consumers_sync();
+      return;
+    }
     if (old % (unsigned long long)P == (unsigned long long)(P - 1)) {   // last arrival: release all
       for (int cc = lane; cc < P; cc += 32)
         asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(bar + 16 * (1 + cc)), "l"(ep) : "memory");
@@ -498,6 +517,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
             prefetch_l2(lw.p_w2 + o, (uint32_t)min((size_t)32768, a1 - o), keep);
         }
       };
+      if (!(p.knobs & 16)) {
+        // the small per-layer vectors the consumers read first (b1: every CTA, b2: my slice)
+        // would cost an HBM round trip at the start of the layer: pull them into L2 now
+        const uint64_t keep = policy_evict_last();
+        if (lw.p_b1 && c == 0) prefetch_l2(lw.p_b1, (uint32_t)(((size_t)r * 2 + 15) & ~(size_t)15), keep);
+        if (lw.p_b2) {
+          const size_t a0 = ((size_t)w0 * 64) & ~(size_t)15;
+          const size_t a1 = min((size_t)m * 2 & ~(size_t)15, ((size_t)min(m, w1 * 32) * 2 + 15) & ~(size_t)15);
+          if (a1 > a0) prefetch_l2((const uint8_t *)lw.p_b2 + a0, (uint32_t)(a1 - a0), keep);
+        }
+      }
       for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
         prefetch_tail(st);
         const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
@@ -663,7 +693,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
     }
     if (tr && tid == 0) tr[1] = globaltimer();
-    grid_sync(p.bar, P, tr ? tr + 204 : nullptr);
+    grid_sync(p.bar, P, tr ? tr + 204 : nullptr, p.knobs & 8);
     if (tr && tid == 0) tr[2] = globaltimer();
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
@@ -678,7 +708,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     }
     consumers_sync();
     if (tid == 0) p.counts[c] = s_count;
-    grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
+    grid_sync(p.bar, P, tr ? tr + 212 : nullptr, p.knobs & 8);
     if (tr && tid == 0) tr[4] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
@@ -892,7 +922,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     ring = it_ffn + n_st;
 
     if (tr && tid == 0) tr[6] = globaltimer();
-    grid_sync(p.bar, P, tr ? tr + 208 : nullptr);
+    grid_sync(p.bar, P, tr ? tr + 208 : nullptr, p.knobs & 8);
     if (tr && tid == 0) tr[7] = globaltimer();
 
     // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
@@ -926,7 +956,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
     }
     if (tr && tid == 0) tr[8] = globaltimer();
-    if (l < L - 1) grid_sync(p.bar, P, tr ? tr + 216 : nullptr);   // the next layer reads all of y
+    if (l < L - 1) grid_sync(p.bar, P, tr ? tr + 216 : nullptr, p.knobs & 8);   // the next layer reads all of y
   }
 }
 

@@ -132,8 +132,26 @@ __global__ void __launch_bounds__(576, 1) k_bar(unsigned long long *bar, int ite
       for (uint32_t j = (it > (uint32_t)NS ? it - NS : 0); j < it; ++j)
         while (!mbar_try(&full[j % NS], (j / NS) & 1)) {}
     };
+    if (stream == 4) {
+      unsigned long long tn;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+      while (!*(volatile int *)stop) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t < tn) continue;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(base + off), "r"(32768u) : "memory");
+        off += SB;
+        if (off + SB > per) off = 0;
+        tn += 740;
+      }
+      return;
+    }
+    const int depth = stream == 1 ? NS : stream == 2 ? 2 : 1;
     for (uint32_t it = 0;; ++it) {
       const int s = it % NS;
+      if (it >= (uint32_t)depth)
+        while (!mbar_try(&full[(it - depth) % NS], ((it - depth) / NS) & 1))
+          if (*(volatile int *)stop) { drain(it); return; }
       if (it >= NS)
         while (!mbar_try(&empty[s], ((it / NS) - 1) & 1))
           if (*(volatile int *)stop) { drain(it); return; }
@@ -145,7 +163,7 @@ __global__ void __launch_bounds__(576, 1) k_bar(unsigned long long *bar, int ite
     }
   }
   if (warp == 17) {
-    if (!stream || lane) return;
+    if (!stream || stream == 4 || lane) return;
     for (uint32_t it = 0;; ++it) {
       const int s = it % NS;
       while (!mbar_try(&full[s], (it / NS) & 1))
@@ -214,8 +232,8 @@ int main() {
   const int iters = 2008;
   printf("P=%d; us per barrier (max over CTAs)\n", P);
   for (int stf : {0, 8192})
-    for (int stream : {0, 1})
-      for (int ns : {0, 32, 100}) {
+    for (int stream : {0, 1, 2, 3, 4})
+      for (int ns : {32}) {
         float v0 = run<0>(bar, iters, ns, stream, src, sb, scr, stf, out, stop, P);
         float v1 = run<1>(bar, iters, ns, stream, src, sb, scr, stf, out, stop, P);
         float v2 = run<2>(bar, iters, ns, stream, src, sb, scr, stf, out, stop, P);
