@@ -73,6 +73,23 @@ __global__ void __launch_bounds__(576, 1) k(const uint8_t *src, size_t src_bytes
       mbar_arrive(&empty[s]);
     }
   }
+  if (MODE == 2) {
+    // dependent shared-load chain (latency): idx = cbuf32[idx], 64 KB region, stride 1 KB + 4 B
+    uint32_t *c32 = (uint32_t *)cbuf;
+    for (int i = tid; i < 2 * SB / 4; i += 512) c32[i] = (uint32_t)((i + 257) % (2 * SB / 4));
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    uint32_t idx = (uint32_t)(warp * 64 + lane);
+    const long long c0 = clock64();
+    for (int itr = 0; itr < iters; ++itr) {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(idx) : "r"(sa(c32 + idx)));
+    }
+    const long long c1 = clock64();
+    if (lane == 0) cyc[blockIdx.x * 16 + warp] = (unsigned long long)(c1 - c0);
+    if (idx == 0xffffffffu) out[tid] = 1.f;
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    if (tid == 0) atomicAdd(stop, 1);
+    return;
+  }
   // compute warps: each iteration, 4 rows of r = 512 bf16 from cbuf (row-major, 1 KB rows)
   float g[2][8];
   for (int q = 0; q < 2; ++q)
@@ -141,8 +158,11 @@ void run(const uint8_t *src, size_t sb, int stream, int iters, float *out, unsig
   for (int i = 0; i < P * 16; ++i) s += h[i];
   const double per_it = s / (P * 16) / iters;
   // bytes read per iteration by all 16 warps of a CTA: 16 * 4 rows * 1 KB
-  printf("mode %d stream %d : %.0f cycles per iteration per warp -> %.1f B/clk/SM of LDS\n", MODE, stream, per_it,
-         16.0 * 4096 / per_it);
+  if (MODE == 2)
+    printf("mode 2 stream %d : dependent LDS latency %.1f cycles (16 warps chasing)\n", stream, per_it);
+  else
+    printf("mode %d stream %d : %.0f cycles per iteration per warp -> %.1f B/clk/SM of LDS\n", MODE, stream, per_it,
+           16.0 * 4096 / per_it);
   fflush(stdout);
 }
 
@@ -162,6 +182,7 @@ int main() {
   for (int stream : {0, 1}) {
     run<0>(src, sb, stream, 2000, out, cyc, stop, P, 16);
     run<1>(src, sb, stream, 2000, out, cyc, stop, P, 16);
+    run<2>(src, sb, stream, 20000, out, cyc, stop, P, 16);
   }
   return 0;
 }
