@@ -417,7 +417,8 @@ def test_full_size_layers(env, name):
 
 
 @pytest.mark.parametrize("name,dims,B", [("c4", (2048, 3000, 64), 1), ("c3", (1024, 2000, 64), 2),
-                                         ("c1", (768, 3072, 64), 1), ("c5", (12288, 700, 64), 1)])
+                                         ("c1", (768, 3072, 64), 1), ("c5", (12288, 700, 64), 1),
+                                         ("c4", (8192, 32768, 512), 1)])   # full c4 layers: the bench's kernel
 def test_stack_kernel_equals_layer_chain(env, name, dims, B):
     """pi_stack_run (one persistent launch for all layers) == chaining pi_layer_forward, bit for bit,
     and every layer matches the oracle on its own input."""
