@@ -48,9 +48,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0, help="CPU budget of the oracle baseline")
-    ap.add_argument("--hot-freq", type=float, default=0.0,
-                    help="L2-prefetch neurons with activation frequency >= this (<= 0 disables; measured "
-                         "slower on c4: 2.61 ms/step at 0.9 vs 2.53 off)")
+    ap.add_argument("--hot-freq", type=float, default=0.99,
+                    help="hot neurons (Insight-1): the fused kernel L2-prefetches the rows of up to PI_HOT_CAP "
+                         "(default 512) neurons per layer whose profiled activation frequency is >= this, "
+                         "while the layer synchronises after phase 2 (<= 0 disables; c4: 2.22 vs 2.30 ms/step)")
     return ap.parse_args()
 
 
@@ -196,17 +197,19 @@ def run_reference(args, cfg, B, n_layers):
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "impl": "reference", "config": workload_config(cfg, B, n_layers, args.gpus),
+           "impl": "reference", "config": workload_config(cfg, B, n_layers, args.gpus, hot_freq=args.hot_freq),
            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def workload_config(cfg, B, n_layers, N, extra=None):
+def workload_config(cfg, B, n_layers, N, extra=None, hot_freq=0.0):
     c = {"workload": f"{cfg.name}: {cfg.desc}", "d": cfg.d, "ffn": cfg.m, "predictor_rank": cfg.r,
          "layers": n_layers, "batch": B, "act": cfg.act, "weights": cfg.dtype, "activations": "fp32",
          "mean_activity_target": 0.10, "mask_mode": "P (predictor-generated, planted b2)",
-         "parallelism": "single GPU" if N == 1 else f"neuron-sharded x{N} (pi_partition) + NCCL all-reduce"}
+         "parallelism": "single GPU" if N == 1 else f"neuron-sharded x{N} (pi_partition) + NCCL all-reduce",
+         "hot_neurons": ("L2 prefetch of <= %s neurons/layer with profiled frequency >= %g" %
+                         (os.environ.get("PI_HOT_CAP", "512"), hot_freq)) if hot_freq > 0 else "off"}
     if extra:
         c.update(extra)
     return c
@@ -389,7 +392,7 @@ def main():
                    "l2": ("weights rotated over %d layer copies (> L2)" % copies) if single else
                          "inputs larger than L2 (every step streams %d layers; %.1f GB of FFN weights)" % (
                              n_layers, sum(L.info.weight_bytes for L in stacks[0].layers) / 1e9),
-                   "algorithmic_MB_per_step": round(float(bytes_step.sum(axis=1).mean()) / 1e6, 2)}),
+                   "algorithmic_MB_per_step": round(float(bytes_step.sum(axis=1).mean()) / 1e6, 2)}, hot_freq=args.hot_freq),
                "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
                               "p99": float(np.percentile(per_step, 99))},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -104,6 +104,7 @@ struct FusedParams {
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int knobs;                  // experiment switches (PI_FUSED_KNOBS); 0 = production behaviour
+  int hot_cap;                // at most this many hot neurons are L2-prefetched per layer (PI_HOT_CAP)
 };
 
 // ---------------------------------------------------------------------------
@@ -440,6 +441,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint64_t *empty = full + NS;
   uint64_t *hready = empty + NS;
   uint64_t *ids_ready = hready + NS;
+  uint64_t *p2_done = ids_ready + 1;   // this CTA's phase 2 has finished (hot-neuron prefetch trigger)
   float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][8][32]
   float *hs = red + 2 * kGroupWarps * kRedStride;                    // [NS][NA*B]
   float *zbuf = hs + NS * NA * B;                                    // [B][wcap*32] logits of my words
@@ -473,6 +475,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_init(&hready[s], 1);
     }
     mbar_init(ids_ready, 1);
+    mbar_init(p2_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -547,11 +550,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
       }
       if (lw.n_hot) {
-        // hot neurons (activation frequency >= hot_freq) are almost surely active: pull this
-        // CTA's share of their up/down rows into L2 now, while the layer runs its predictor and
-        // synchronises; the FFN phase then streams them from L2
+        // hot neurons (activation frequency >= hot_freq) are almost surely active: once this
+        // CTA's phase 2 is done (its P2 stages are in, HBM idles through barrier 2 and the
+        // compaction), pull this CTA's share of the first p.hot_cap of their up/down rows into
+        // L2; the FFN stages of those neurons then load from L2
+        mbar_wait(p2_done, l & 1);
         const uint64_t keep = policy_evict_last();
-        for (int k = c; k < lw.n_hot; k += P) {
+        const int nh = min(lw.n_hot, p.hot_cap);
+        for (int k = c; k < nh; k += P) {
           const int i = lw.hot_ids[k];
           prefetch_l2(lw.w_up + (size_t)i * row_up, (uint32_t)row_up, keep);
           prefetch_l2(lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, keep);
@@ -707,7 +713,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       else p2_phase<T, B, 4>(ctx);
     }
     consumers_sync();
-    if (tid == 0) p.counts[c] = s_count;
+    if (tid == 0) {
+      p.counts[c] = s_count;
+      mbar_arrive(p2_done);
+    }
     grid_sync(p.bar, P, tr ? tr + 212 : nullptr, p.knobs & 8);
     if (tr && tid == 0) tr[4] = globaltimer();
 
@@ -1097,6 +1106,8 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   {
     const char *e = getenv("PI_FUSED_KNOBS");
     p.knobs = e ? atoi(e) : 0;
+    const char *h = getenv("PI_HOT_CAP");
+    p.hot_cap = h ? atoi(h) : 512;
   }
   return p;
 }

@@ -452,3 +452,27 @@ def test_stack_kernel_equals_layer_chain(env, name, dims, B):
         torch.cuda.synchronize()
         assert torch.equal(y2, y)
     S.close()
+
+
+def test_hot_neuron_prefetch_changes_nothing(env):
+    """Hot-neuron L2 prefetch (neuron_freq / hot_freq, Insight-1) only moves data: the stack kernel's
+    output with the prefetch on is bitwise identical to the output with it off."""
+    gen, pi = env
+    cfg = gen.CONFIGS["c4"]
+    d, m, r = 2048, 4096, 64
+    flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
+    ws = [gen.make_layer(cfg, layer=l, seed=5, device="cuda", d=d, m=m, r=r) for l in range(3)]
+    x = gen.tokens(1, d, seed=6, device="cuda")
+    outs = []
+    for hot in (None, 0.5):
+        Ls = [pi.Layer(w, max_batch=1, flags=flags, layer_id=l,
+                       neuron_freq=None if hot is None else w.p, hot_freq=hot if hot else 0.9)
+              for l, w in enumerate(ws)]
+        S = pi.StackHandle(Ls)
+        y = torch.empty(1, d, device="cuda")
+        for _ in range(3):
+            S.run(x, y)
+        torch.cuda.synchronize()
+        outs.append(y.clone())
+        S.close()
+    assert torch.equal(outs[0], outs[1])
