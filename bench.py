@@ -3,6 +3,11 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl pi|reference]
 
+With --gpus N > 1 and no torchrun environment (WORLD_SIZE unset), bench.py re-launches itself
+under ``torch.distributed.run --nproc-per-node N`` (127.0.0.1 rendezvous), one rank per GPU.
+``--dry-run`` exercises the multi-rank plumbing (spawn, rendezvous, the per-layer collective,
+max-over-ranks timing, the JSON line) on CPU with gloo and no kernels: its numbers mean nothing.
+
 One step = one decode token (batch B) through every layer of the workload: the whole hot
 path of SURVEY.md 8(a) (predictor -> mask -> compaction -> row-sparse up -> column-sparse
 down [-> NCCL all-reduce for N > 1]).  Default workload: configs[3] of BASELINE.json, the
@@ -49,10 +54,42 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=15.0, help="CPU budget of the oracle baseline")
     ap.add_argument("--hot-freq", type=float, default=0.99,
-                    help="hot neurons (Insight-1): the fused kernel L2-prefetches the rows of up to PI_HOT_CAP "
-                         "(default 512) neurons per layer whose profiled activation frequency is >= this, "
-                         "while the layer synchronises after phase 2 (<= 0 disables; c4: 2.22 vs 2.30 ms/step)")
+                    help="hot neurons (Insight-1): the fused kernel L2-prefetches the rows of up to --hot-cap "
+                         "neurons per layer whose profiled activation frequency is >= this, while the layer "
+                         "synchronises after phase 2 (<= 0 disables; c4: 2.22 vs 2.30 ms/step)")
+    ap.add_argument("--hot-cap", type=int, default=512, help="hot neurons prefetched per layer (pi_layer_desc.hot_cap)")
+    ap.add_argument("--mean-act", type=float, default=0.10, help="mean activity of the planted profile (5-20%%)")
+    ap.add_argument("--rank", dest="pred_rank", type=int, default=None, help="predictor rank r override")
+    ap.add_argument("--no-phases", action="store_true", help="skip the traced per-phase breakdown pass")
+    ap.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no kernels (numbers meaningless)")
     return ap.parse_args()
+
+
+def maybe_spawn(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run, one rank per GPU."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def host_cores():
+    """Host core counts the CPU legs can use (cpu_count, affinity, BLAS threads)."""
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        blas = max((p.get("num_threads", 0) for p in threadpool_info()), default=None)
+    except Exception:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": aff, "blas_threads": blas, "torch_threads": torch.get_num_threads()}
 
 
 # ---------------------------------------------------------------------------
@@ -123,45 +160,76 @@ def hbm_peak():
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (TEST/BASELINE leg only: the one place bench.py runs oracle/)
 # ---------------------------------------------------------------------------
-def oracle_baseline(cfg, seed, n_layers_total, B, seconds, device):
-    """Time oracle predict -> compact -> sparse_ffn on host cores for a bounded sample."""
+def _oracle_layer_step(O, W, x, cfg, t):
+    xo = O.rms_normalize(x) if cfg.rmsnorm else x
+    mask, _ = O.predict(xo, W["p_w1"], W["p_b1"], W["p_w2"], W["p_b2"], t)
+    ids = O.compact(mask)
+    O.sparse_ffn(xo, ids, mask, W["w_up"], W["b_up"], W["w_gate"], W["w_down"], W["b_down"], cfg.act)
+
+
+def _oracle_time(O, Ws, cfg, B, seed, seconds, max_samples=64):
+    """Mean seconds per (token-batch, layer) over a bounded sample (time-boxed, >= 2 samples/layer)."""
+    ts = []
+    for l, W in enumerate(Ws):
+        tok = 0
+        while True:
+            from paper_2312_12456_b200 import gen
+            x = gen.tokens(B, cfg.d, seed=seed + 99, step=tok, device="cpu").numpy().astype(np.float64)
+            t0 = time.perf_counter()
+            _oracle_layer_step(O, W, x, cfg, W["t"])
+            ts.append(time.perf_counter() - t0)
+            tok += 1
+            if (tok >= 2 and sum(ts) > seconds * (l + 1) / len(Ws)) or tok >= max_samples:
+                break
+    return float(np.mean(ts)), len(ts)
+
+
+def _threads(n):
+    """Cap NumPy's BLAS and torch's intra-op threads at n (threadpoolctl when present)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=n)
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def oracle_baseline(cfg, seed, n_layers_total, B, seconds, device, dims=None):
+    """Time oracle predict -> compact -> sparse_ffn on host cores for a bounded sample: once with
+    one thread and once with every core of this process's affinity set."""
     from oracle import ffn as O
     from paper_2312_12456_b200 import gen
 
     k = 2 if n_layers_total > 1 else 1
-    t_layer = []
-    samples = 0
     t_start = time.perf_counter()
+    Ws = []
     for l in range(k):
-        w = gen.make_layer(cfg, layer=l, seed=seed, device=device)
+        w = gen.make_layer(cfg, layer=l, seed=seed, device=device, **(dims or {}))
         f = lambda t: None if t is None else t.float().cpu().numpy()  # noqa: E731
         W = {kk: f(v) for kk, v in w.tensors().items()}
+        W["t"] = w.threshold
+        Ws.append(W)
         del w
-        tok = 0
-        while True:
-            x = gen.tokens(B, cfg.d, seed=seed + 99, step=tok, device="cpu").numpy().astype(np.float64)
-            t0 = time.perf_counter()
-            xo = O.rms_normalize(x) if cfg.rmsnorm else x
-            mask, _ = O.predict(xo, W["p_w1"], W["p_b1"], W["p_w2"], W["p_b2"], 0.0)
-            ids = O.compact(mask)
-            O.sparse_ffn(xo, ids, mask, W["w_up"], W["b_up"], W["w_gate"], W["w_down"], W["b_down"], cfg.act)
-            t_layer.append(time.perf_counter() - t0)
-            tok += 1
-            samples += 1
-            if sum(t_layer) > seconds * (l + 1) / k or tok >= 64:
-                break
-        del W
-    per_layer = float(np.mean(t_layer))
-    value = B / (per_layer * n_layers_total)
-    return {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-            "sample": f"{samples} (token-batch, layer) pairs over layers 0..{k - 1} of {n_layers_total}, "
-                      f"B={B}; full-stack time extrapolated x{n_layers_total}; numpy fp64 single-threaded "
-                      f"(elementwise ops, no BLAS in the timed path); weight generation and host copies untimed",
-            "seconds": round(time.perf_counter() - t_start, 1)}
+    cores = host_cores()
+    with _threads(1):
+        per1, n1 = _oracle_time(O, Ws, cfg, B, seed, seconds / 2)
+    with _threads(cores["affinity"]):
+        perN, nN = _oracle_time(O, Ws, cfg, B, seed, seconds / 2)
+    best_cores, per = (1, per1) if per1 <= perN else (cores["affinity"], perN)
+    return {"value": B / (per * n_layers_total), "unit": "tokens/s", "cores": best_cores, "kind": "oracle",
+            "sample": f"{n1} + {nN} (token-batch, layer) pairs over layers 0..{k - 1} of {n_layers_total}, B={B}, "
+                      f"timed with 1 thread and with {cores['affinity']} threads; value = the faster, full-stack "
+                      f"time extrapolated x{n_layers_total}; numpy fp64; weight generation and host copies untimed",
+            "one_thread_tokens_s": B / (per1 * n_layers_total),
+            "all_cores_tokens_s": B / (perN * n_layers_total),
+            "ms_per_layer_one_thread": per1 * 1e3, "ms_per_layer_all_cores": perN * 1e3,
+            "host": cores, "seconds": round(time.perf_counter() - t_start, 1)}
 
 
 def run_reference(args, cfg, B, n_layers):
-    """--impl reference: the oracle as it stands on the host cores, same config/metric/unit."""
+    """--impl reference: the oracle as it stands on the host cores, same config/metric/unit.  One
+    step here = one token-batch through ONE layer (a bounded sample of the workload);
+    ms_per_step is that measured time, and the metric value extrapolates it x n_layers."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -171,53 +239,134 @@ def run_reference(args, cfg, B, n_layers):
     k = min(2, n_layers)
     Ws = []
     for l in range(k):
-        w = gen.make_layer(cfg, layer=l, seed=args.seed, device="cpu")
+        w = gen.make_layer(cfg, layer=l, seed=args.seed, device="cpu", **layer_dims(args))
         f = lambda t: None if t is None else t.float().numpy()  # noqa: E731
-        Ws.append({kk: f(v) for kk, v in w.tensors().items()})
+        W = {kk: f(v) for kk, v in w.tensors().items()}
+        W["t"] = w.threshold
+        Ws.append(W)
         del w
+    cores = host_cores()
 
     def one(step):
         W = Ws[step % k]
         x = gen.tokens(B, cfg.d, seed=args.seed, step=step, device="cpu").numpy().astype(np.float64)
         t0 = time.perf_counter()
-        xo = O.rms_normalize(x) if cfg.rmsnorm else x
-        mask, _ = O.predict(xo, W["p_w1"], W["p_b1"], W["p_w2"], W["p_b2"], 0.0)
-        ids = O.compact(mask)
-        O.sparse_ffn(xo, ids, mask, W["w_up"], W["b_up"], W["w_gate"], W["w_down"], W["b_down"], cfg.act)
+        _oracle_layer_step(O, W, x, cfg, W["t"])
         return time.perf_counter() - t0
 
-    for i in range(args.warmup):
-        one(i)
-    ts = [one(args.warmup + i) for i in range(args.steps)]
+    with _threads(cores["affinity"]):
+        for i in range(args.warmup):
+            one(i)
+        ts = [one(args.warmup + i) for i in range(args.steps)]
     per_layer = float(np.mean(ts))
-    ms_step = per_layer * n_layers * 1e3
     value = B / (per_layer * n_layers)
-    sample = (f"each step = one token-batch (B={B}) through one of layers 0..{k - 1}; per-step time extrapolated "
-              f"x{n_layers} layers; numpy fp64, single thread")
+    sample = (f"each step = one token-batch (B={B}) through one of layers 0..{k - 1} (measured); tokens/s = "
+              f"B / (mean step time x {n_layers} layers) (extrapolated); numpy fp64, {cores['affinity']} threads")
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+           "warmup": args.warmup, "ms_per_step": per_layer * 1e3, "step": "one token-batch through one layer",
+           "ms_per_token_extrapolated": per_layer * n_layers * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "impl": "reference", "config": workload_config(cfg, B, n_layers, args.gpus, hot_freq=args.hot_freq),
-           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle", "sample": sample},
+           "impl": "reference", "config": workload_config(cfg, B, n_layers, args.gpus, args=args),
+           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores["affinity"], "kind": "oracle",
+                            "sample": sample, "host": cores},
            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def workload_config(cfg, B, n_layers, N, extra=None, hot_freq=0.0):
-    c = {"workload": f"{cfg.name}: {cfg.desc}", "d": cfg.d, "ffn": cfg.m, "predictor_rank": cfg.r,
+def layer_dims(args):
+    return {"r": args.pred_rank} if args.pred_rank else {}
+
+
+def workload_config(cfg, B, n_layers, N, extra=None, args=None):
+    hot_freq = args.hot_freq if args is not None else 0.0
+    c = {"workload": f"{cfg.name}: {cfg.desc}", "d": cfg.d, "ffn": cfg.m,
+         "predictor_rank": (args.pred_rank if args is not None and args.pred_rank else cfg.r),
          "layers": n_layers, "batch": B, "act": cfg.act, "weights": cfg.dtype, "activations": "fp32",
-         "mean_activity_target": 0.10, "mask_mode": "P (predictor-generated, planted b2)",
+         "mean_activity_target": args.mean_act if args is not None else 0.10,
+         "mask_mode": "P (predictor-generated, planted b2)",
          "parallelism": "single GPU" if N == 1 else f"neuron-sharded x{N} (pi_partition) + NCCL all-reduce",
-         "hot_neurons": ("L2 prefetch of <= %s neurons/layer with profiled frequency >= %g" %
-                         (os.environ.get("PI_HOT_CAP", "512"), hot_freq)) if hot_freq > 0 else "off"}
+         "hot_neurons": ("L2 prefetch of <= %d neurons/layer with profiled frequency >= %g" %
+                         (args.hot_cap, hot_freq)) if hot_freq > 0 else "off"}
     if extra:
         c.update(extra)
     return c
 
 
 # ---------------------------------------------------------------------------
+def phase_breakdown(st, x, y, B, n_layers):
+    """One traced (untimed) stack launch: mean over CTAs of each phase of layer 1 (pi_layer_set_trace
+    stamps, include/pi.h), in microseconds.  Barriers are the waits after each phase."""
+    L0 = st.layers[0]
+    P = L0.info.num_sms
+    buf = torch.zeros(P * 256, dtype=torch.int64, device=x.device)
+    L0.set_trace(buf)
+    st.step(x, y, None)
+    torch.cuda.synchronize()
+    L0.set_trace(None)
+    t = buf.view(P, 256)[:, :9].cpu().numpy().astype(np.float64)
+    if (t[:, 0] == 0).any() or (t[:, 8] == 0).any():
+        return None
+    rel = (t - t[:, :1]) / 1e3
+    m = rel.mean(axis=0)
+    names = ["P1 (a1)", "grid barrier 1", "P2 + threshold (a2)", "grid barrier 2", "compaction (a3)",
+             "FFN up+down (a4+a5)", "grid barrier 3", "reduction of partials"]
+    out = {nm: round(float(m[i + 1] - m[i]), 2) for i, nm in enumerate(names)}
+    out["layer_total"] = round(float(m[8]), 2)
+    out["layer_total_max_cta"] = round(float(rel[:, 8].max()), 2)
+    out["source"] = "pi_layer_set_trace stamps of layer 1 of one untimed stack launch, mean over CTAs"
+    return out
+
+
+def dry_run(args, cfg, B, n_layers):
+    """Multi-rank plumbing on CPU (gloo): spawn/rendezvous, the per-layer all-reduce of [B, d]
+    partials, max-over-ranks timing, the JSON line.  No kernels run; the numbers mean nothing."""
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    d = cfg.d
+    x = torch.randn(B, d)
+    bufs = [torch.empty(B, d) for _ in range(2)]
+
+    def step():
+        cur = x
+        for l in range(n_layers):
+            dst = bufs[l & 1]
+            dst.copy_(cur)
+            if world > 1:
+                dist.all_reduce(dst)
+            cur = dst
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    if world > 1:
+        dist.barrier()
+    total = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([total])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total = float(t.item())
+    if rank == 0:
+        out = {"metric": METRIC, "value": B * args.steps / total, "unit": "tokens/s", "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+               "data": "synthetic", "dry_run": True,
+               "config": workload_config(cfg, B, n_layers, world, {"note": "CPU gloo plumbing check, no kernels"},
+                                         args=args)}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
+    maybe_spawn(args)
     from paper_2312_12456_b200 import gen
 
     cfg = gen.CONFIGS[args.config]
@@ -226,9 +375,11 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, B, n_layers)
         return
+    if args.dry_run:
+        dry_run(args, cfg, B, n_layers)
+        return
 
     import torch.distributed as dist
-    from paper_2312_12456_b200 import pi
     from paper_2312_12456_b200.stack import algorithmic_bytes, build_stack
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,26 +398,36 @@ def main():
     stacks = []
     for c in range(copies):
         st, _ = build_stack(cfg, n_layers=n_layers, rank=rank, world=world, seed=args.seed + 1000 * c,
-                            device=dev, max_batch=B, group=group,
-                            hot_freq=args.hot_freq if args.hot_freq > 0 else None)
+                            device=dev, max_batch=B, group=group, mean_act=args.mean_act, dims=layer_dims(args),
+                            hot_freq=args.hot_freq if args.hot_freq > 0 else None, hot_cap=args.hot_cap)
         stacks.append(st)
     d = cfg.d
     T = args.warmup + args.steps
     xs = torch.stack([gen.tokens(B, d, seed=args.seed + 7, step=i, device=dev) for i in range(T)])
     y = torch.empty(B, d, device=dev)
-    bufs = [torch.empty(B, d, device=dev) for _ in range(2)]
     nbuf = torch.zeros(T, n_layers, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
+    graphs = None
+    if world > 1:
+        # the sharded step (per layer: fused kernel + NCCL all-reduce) replays as one CUDA graph
+        xg = torch.empty(B, d, device=dev)
+        ng = torch.zeros(n_layers, dtype=torch.int32, device=dev)
+        graphs = [st.capture(xg, y, ng) for st in stacks]
 
-    def step(i, record_n=True):
+    def step(i):
         st = stacks[i % copies]
-        st.step(xs[i], y, nbuf[i] if record_n else None, bufs)
+        if graphs is None:
+            st.step(xs[i], y, nbuf[i])
+        else:
+            xg.copy_(xs[i])
+            graphs[i % copies].replay()
+            nbuf[i].copy_(ng)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # ---- warm-up, then EXACTLY K timed steps ----
+    # ---- warm-up, then EXACTLY K timed steps (one event per step boundary on the launching stream) ----
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -300,49 +461,48 @@ def main():
     realised = float(n_host.mean() / metas[0].m_local)
 
     # ---- dominant kernel: per-launch durations with CUDA events on the launching stream ----
-    # world 1: the stack kernel (one launch = one step through every layer);
-    # world > 1: the per-layer fused kernel (launches separated by the NCCL all-reduce)
-    prof_steps = min(args.steps, 10)
-    kt, kb = [], []
-    for k in range(prof_steps):
-        i = args.warmup + k
-        st = stacks[i % copies]
-        if world == 1:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            st.step(xs[i], y, None, bufs)
-            e1.record(stream)
+    launches_per_layer = int(stacks[0].layers[0].info.launches_per_forward)
+    one_launch = world == 1 and launches_per_layer == 1 and not single
+    if world == 1 and launches_per_layer == 1:
+        # world 1: every timed step IS one launch of the fused kernel (pi_stack_run: all layers; single-layer
+        # configs: one layer), so the per-step events of the timed loop are per-launch durations
+        kt = per_step / 1e3
+        kb = bytes_step.sum(axis=1)
+        timing_src = "CUDA events around each launch inside the timed loop"
+    else:
+        kt, kb = [], []
+        for k in range(min(args.steps, 10)):
+            i = args.warmup + k
+            st = stacks[i % copies]
+            e0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
+            e1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
+            cur = xs[i]
+            bufs = st._bufs(cur)
+            for l, L in enumerate(st.layers):
+                dst = bufs[l & 1]
+                e0[l].record(stream)
+                L.forward(cur, dst)
+                e1[l].record(stream)
+                if world > 1:
+                    dist.all_reduce(dst)
+                cur = dst
             torch.cuda.synchronize()
-            kt.append(e0.elapsed_time(e1) / 1e3)
-            kb.append(float(bytes_step[k].sum()))
-            continue
-        e0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
-        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
-        cur = xs[i]
-        for l, L in enumerate(st.layers):
-            dst = bufs[l & 1]
-            e0[l].record(stream)
-            L.forward(cur, dst)
-            e1[l].record(stream)
-            dist.all_reduce(dst)
-            cur = dst
-        torch.cuda.synchronize()
-        for l in range(n_layers):
-            kt.append(e0[l].elapsed_time(e1[l]) / 1e3)
-            kb.append(algorithmic_bytes(metas[l], int(n_host[k, l]), B))
+            for l in range(n_layers):
+                kt.append(e0[l].elapsed_time(e1[l]) / 1e3)
+                kb.append(algorithmic_bytes(metas[l], int(n_host[k, l]), B))
+        timing_src = "CUDA events around each layer's launch in a separate 10-step pass"
     launch_s = float(np.mean(kt))
     bytes_launch = float(np.mean(kb))
     peak, peak_src = hbm_peak()
     achieved = bytes_launch / launch_s / 1e9
-    launches_per_layer = int(stacks[0].layers[0].info.launches_per_forward)
-    kname = ("k_layer x%d layers in one persistent launch (pi_stack_run)" % n_layers) if world == 1 and \
-        launches_per_layer == 1 else "pi_layer_forward (%d launch(es) per layer)" % launches_per_layer
+    kname = ("k_layer x%d layers in one persistent launch (pi_stack_run)" % n_layers) if one_launch else \
+        "pi_layer_forward (%d launch(es) per layer)" % launches_per_layer
     launches_per_step = 1 if (world == 1 and launches_per_layer == 1) else n_layers * launches_per_layer
     traffic, traffic_src = None, None
     try:   # DRAM bytes / algorithmic bytes from the committed ncu --set full capture of this kernel
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        if world == 1 and args.config == "c4":
+        if one_launch and args.config == tj.get("config", "c4") and B == tj.get("batch", 1):
             traffic = int(tj["ratio"] * bytes_launch)
             traffic_src = "%s (ratio %.3f of algorithmic bytes, scaled to this launch)" % (tj["capture"], tj["ratio"])
     except Exception:
@@ -350,8 +510,15 @@ def main():
     roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
-                "bytes_per_launch": int(bytes_launch), "launch_us": round(launch_s * 1e6, 2),
+                "bytes_per_launch": int(bytes_launch), "launch_us": round(launch_s * 1e6, 2), "timing": timing_src,
                 "step_frac": round(float(bytes_step.sum(axis=1).mean()) / (ms_per_step / 1e3) / 1e9 / peak, 4)}
+
+    phases = None
+    if world == 1 and one_launch and not args.no_phases:
+        try:
+            phases = phase_breakdown(stacks[0], xs[0], y, B, n_layers)
+        except Exception as e:  # tracing is diagnostic only
+            phases = {"error": repr(e)}
 
     # ---- e2e through the public C ABI with host buffers ----
     e2e = None
@@ -366,8 +533,8 @@ def main():
             if world == 1:
                 st.stack.run_host(xh[i], yh)
             else:
-                xd = xh[i].to(dev, non_blocking=True)
-                st.step(xd, y, None, bufs)
+                xg.copy_(xh[i], non_blocking=True)
+                graphs[i % copies].replay()
                 yh.copy_(y, non_blocking=True)
                 torch.cuda.current_stream().synchronize()
         e2e_s = time.perf_counter() - t0
@@ -377,11 +544,11 @@ def main():
             e2e_s = float(t.item())
         e2e = {"value": B * args.steps / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": B * d * 4,
                "d2h_bytes_per_step": B * d * 4, "api": "pi_stack_run_host" if world == 1 else
-               "host copy + pi_layer_forward + NCCL all_reduce per layer + host copy"}
+               "host copy + CUDA-graph replay of (pi_layer_forward + NCCL all_reduce) x layers + host copy"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_baseline(cfg, args.seed, n_layers, B, args.ref_seconds, dev)
+        cpu = oracle_baseline(cfg, args.seed, n_layers, B, args.ref_seconds, dev, layer_dims(args))
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -392,10 +559,10 @@ def main():
                    "l2": ("weights rotated over %d layer copies (> L2)" % copies) if single else
                          "inputs larger than L2 (every step streams %d layers; %.1f GB of FFN weights)" % (
                              n_layers, sum(L.info.weight_bytes for L in stacks[0].layers) / 1e9),
-                   "algorithmic_MB_per_step": round(float(bytes_step.sum(axis=1).mean()) / 1e6, 2)}, hot_freq=args.hot_freq),
+                   "algorithmic_MB_per_step": round(float(bytes_step.sum(axis=1).mean()) / 1e6, 2)}, args=args),
                "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
                               "p99": float(np.percentile(per_step, 99))},
-               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline, "phases_us": phases, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(args.steps * launches_per_step), "clocks": clk}
         print(json.dumps(out), flush=True)
     if world > 1:

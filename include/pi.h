@@ -67,6 +67,8 @@ typedef enum { PI_PRED_RELU = 0, PI_PRED_LINEAR = 1 } pi_pred_act;
 #define PI_FLAG_MULTI_KERNEL 2u
 
 #define PI_MAX_BATCH 8
+/* default for pi_layer_desc.hot_cap (hot neurons L2-prefetched per layer and step) */
+#define PI_DEFAULT_HOT_CAP 512
 
 /* Layer description.  Weight pointers are DEVICE pointers in the PyTorch
  * nn.Linear layouts of the GLOBAL layer (m_total neurons); the handle keeps the
@@ -99,9 +101,12 @@ typedef struct {
    * P:680-690) of the GLOBAL layer, host [m_total], or NULL.  Neurons of this shard with
    * f_i >= hot_freq are "hot": while the layer runs its predictor and synchronises, the fused
    * kernel pulls their up/down rows into L2 so the FFN phase streams them from L2 instead of
-   * HBM.  Results are unchanged (hotness only affects data movement). */
+   * HBM.  Results are unchanged (hotness only affects data movement).  Hot neurons are ranked
+   * by (-f_i, id); at most hot_cap of them (<= 0: PI_DEFAULT_HOT_CAP) are prefetched per step,
+   * the hottest first. */
   const float *neuron_freq;
   float hot_freq;
+  int32_t hot_cap;
 } pi_layer_desc;
 
 typedef struct {
@@ -196,7 +201,10 @@ pi_status pi_stack_forward_host(pi_layer *const *layers, int32_t n_layers, const
  * max_batch) run as ONE persistent kernel per decode step, x_{l+1} = y_l.  The kernel's TMA
  * producer streams layer l+1's predictor rows while layer l finishes, and no launch gap
  * separates the layers.  The stack keeps pointers to the layers (it does not own them);
- * destroy the stack before its layers.  Errors: INVALID_ARGUMENT, SHAPE (incompatible
+ * destroy the stack before its layers.  A stack run uses layer 0's workspace (the fused
+ * kernel's grid barrier, mask, partials and the host-staging buffers), so it counts as the
+ * one call in flight on layer 0's handle: do not run layer 0 (or another stack that starts
+ * with it) concurrently.  Errors: INVALID_ARGUMENT, SHAPE (incompatible
  * layers), OUT_OF_MEMORY, CUDA. */
 typedef struct pi_stack pi_stack;
 pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, pi_stack **out);

@@ -1,111 +1,10 @@
-// fused.cuh -- k_layer: the whole hot path of one layer in ONE
-// persistent, cooperative sm_100a kernel.
-//
-// One CTA per SM, 17 warps in three roles:
-//   producer (warp 16) -- one elected lane streams every weight byte the CTA needs (its P1
-//       rows, its block of P2 rows, then the up(/gate) and down rows of its share of the
-//       active neurons) with 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) into an
-//       NS-stage shared-memory ring guarded by full/empty mbarriers;
-//   up group (warps 0..7, 256 threads) -- owns x in registers (fixed 16-byte column chunks
-//       of d per thread); computes the P1 row dots and, per ring stage, the up (and gate)
-//       dots of the stage's neurons: per-warp transpose reductions, one 256-thread named
-//       barrier per stage, then h = act(.) is handed to the down group through shared
-//       memory and an "h ready" mbarrier;
-//   down group (warps 8..15, 256 threads) -- computes the P2 GEMV + threshold + ballot
-//       (one warp per ring stage of mask words, transpose-reduced), then, per FFN stage,
-//       accumulates h * down-row into its register-resident partial y.
-// The two groups are decoupled by the ring: the up group runs ahead of the down group.
-//
-//   phase 1  g = act_p(s * P1 x + b1)                rows of P1 dealt round-robin to CTAs
-//   -------- grid barrier 1 (g visible)
-//   phase 2  z = P2 g + b2 ; bit = z > t ; ballot     contiguous block of mask words per CTA
-//            union words + per-CTA popcount
-//   -------- grid barrier 2 (mask, union, counts visible)
-//   phase 3  every CTA prefix-sums the counts, takes compacted positions
-//            [c n / P, (c+1) n / P) -- equal work, since every compacted neuron costs the
-//            same -- extracts its ids from the union words, and streams up + down rows:
-//            h = act(s * W_up[i] x + b_up[i]) (per-token bit), y_part += h * Wd_T[i]
-//   -------- grid barrier 3 (per-CTA partials visible)
-//   phase 4  CTA c reduces its column slice over the P partials in fixed order, + b_down
-//
-// The producer runs ahead across barriers 1 and 2 for P2 rows (data-independent), so those
-// bytes stream in while the grid synchronises.  All reductions have a fixed order: the
-// result is bitwise reproducible run to run; there are no float atomics.
+// fused.cuh -- the k_layer kernel (see fused_host.h for the design notes, parameters and the
+// host-side sizing).  Included only by the fused_inst_*.cu instantiation units.
 #pragma once
 
-#include <algorithm>
-#include <cstdlib>
-
-#include "common.cuh"
+#include "fused_host.h"
 
 namespace pi {
-
-constexpr int kGroupWarps = 8;                        // warps per group (up / down)
-constexpr int kGroup = kGroupWarps * 32;              // 256 threads per group
-constexpr int kConsumerWarps = 2 * kGroupWarps;       // 16
-constexpr int kConsumers = kConsumerWarps * 32;       // 512
-constexpr int kFusedThreads = kConsumers + 32;        // + producer warp
-constexpr int kFusedMaxB = 2;
-constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 16384)
-constexpr int kMaxCG = 4;        // 16-byte chunks of r per lane in phase 2 (r <= 1024)
-constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
-constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
-
-struct FusedWork {
-  bool enabled = false;
-  int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0, part_off = 0, pcap = 0;
-  int d = 0, m = 0, r = 0;
-  bool reglu = false;
-  unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
-  float *g = nullptr;                 // [maxB, r]
-  float *ypart = nullptr;             // [P, maxB, d]
-  int *counts = nullptr;              // [P]
-  uint32_t *mask = nullptr;           // [maxB, words]
-  uint32_t *uni = nullptr;            // [words]
-  float *xbuf = nullptr;              // [maxB, d] inter-layer activations (stack launch)
-  unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
-};
-
-struct FusedArgs {
-  const void *w_up, *w_down, *b_up, *b_down, *p_w1, *p_b1, *p_w2, *p_b2;
-  const float *x;
-  float *y;
-  int d, m, r, words, B;
-  float threshold;
-  bool rmsnorm, pred_relu, reglu;
-  uint32_t *mask_out;
-  int32_t *ids_out, *n_out;
-  const int32_t *hot_ids;
-  int n_hot;
-};
-
-struct LayerW {  // one layer's library-owned weights (device pointers)
-  const uint8_t *w_up, *w_down, *p_w1, *p_w2;
-  const void *b_up, *b_down, *p_b1, *p_b2;
-  const int32_t *hot_ids;   // local ids of the hot neurons (L2-prefetched each step), or NULL
-  int n_hot;
-  float t;
-};
-
-struct FusedParams {
-  LayerW lw0;                 // the layer of a single-layer launch
-  const LayerW *lws;          // device array of L layers (stack launch) or NULL (use lw0)
-  int L;
-  const float *x;             // layer-0 input [B, d]
-  float *y;                   // last-layer output [B, d]
-  float *xbuf;                // inter-layer activations [B, d] (stack launch)
-  int d, m, r, words, B;
-  int rmsnorm, pred_relu;
-  uint32_t *mask, *uni;
-  int32_t *ids_out, *n_out;   // n_out: [L] union counts
-  float *g, *ypart;
-  int *counts;
-  unsigned long long *bar;
-  int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
-  unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
-  int knobs;                  // experiment switches (PI_FUSED_KNOBS); 0 = production behaviour
-  int hot_cap;                // at most this many hot neurons are L2-prefetched per layer (PI_HOT_CAP)
-};
 
 // ---------------------------------------------------------------------------
 // PTX helpers: mbarrier, bulk copy, named barriers, grid barrier
@@ -194,60 +93,31 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
-// Grid barrier over the P co-resident CTAs (cooperative launch).  bar[0] is a monotonic
-// 64-bit arrival counter; bar[16 * (1 + c)] is CTA c's release flag, each on its own 128-byte
-// line.  An arrival that returns `old` belongs to episode e = old / P + 1; the last arrival of
-// the episode writes e into every CTA's flag (warp 0 of that CTA, 32 lanes in parallel), and
-// every CTA polls only its own flag -- no L2 line is polled by 148 SMs at once, so the
-// arrivals are not slowed by the pollers.  A 4-second watchdog traps instead of hanging.
-__device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsigned long long *dbg = nullptr,
-                                          bool flags = false) {
+// Grid barrier over the P co-resident CTAs (cooperative launch).  bar[0] is a monotonic 64-bit
+// arrival counter: an arrival that returns `old` belongs to episode e = old / P + 1, and every
+// CTA polls the counter until it reaches e * P -- one round trip shorter than a flag release by
+// the last arrival (scripts/microbench_barrier.cu: 1.39 vs 1.87 us per barrier on an idle GPU).
+// A 4-second watchdog traps instead of hanging.  dbg (tracing only): cycles to the atomic's
+// return and to the release, and the release time.
+__device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsigned long long *dbg = nullptr) {
   consumers_sync();  // every consumer thread of this CTA has issued its global writes
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    unsigned long long old = 0;
-    long long c0 = clock64();
-    if (lane == 0) {
-      if (dbg) dbg[0] = clock64() - c0;
-      asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
-      if (dbg) dbg[1] = clock64() - c0 + (old == 0xffffffffffffull ? 1 : 0);
-    }
-    old = __shfl_sync(0xffffffffu, old, 0);
-    const unsigned long long ep = old / (unsigned long long)P + 1ull;
-    if (!flags) {
-      // every CTA polls the counter itself: one round trip fewer than a flag release by the
-      // last arrival (scripts/microbench_barrier.cu: 1.39 vs 1.87 us per barrier, idle GPU)
-      if (lane == 0) {
-        const unsigned long long t0 = globaltimer(), target = ep * (unsigned long long)P;
-        while (true) {
-          unsigned long long cur;
-          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
-          if (cur >= target) break;
-          __nanosleep(32);
-          if (globaltimer() - t0 > 4000000000ull) __trap();
-        }
-        if (dbg) dbg[2] = clock64() - c0;
-        if (dbg) dbg[3] = globaltimer();
-      }
-      consumers_sync();
-      return;
-    }
-    if (old % (unsigned long long)P == (unsigned long long)(P - 1)) {   // last arrival: release all
-      for (int cc = lane; cc < P; cc += 32)
-        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(bar + 16 * (1 + cc)), "l"(ep) : "memory");
-    }
-    if (lane == 0) {
-      const unsigned long long *flag = bar + 16 * (1 + blockIdx.x);
-      const unsigned long long t0 = globaltimer();
+  if (threadIdx.x == 0) {
+    const long long c0 = clock64();
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+    if (dbg) dbg[1] = clock64() - c0;
+    const unsigned long long target = (old / (unsigned long long)P + 1ull) * (unsigned long long)P;
+    const unsigned long long t0 = globaltimer();
+    while (true) {
       unsigned long long cur;
-      while (true) {
-        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(flag) : "memory");
-        if (cur >= ep) break;
-        __nanosleep(32);
-        if (globaltimer() - t0 > 4000000000ull) __trap();
-      }
-      if (dbg) dbg[2] = clock64() - c0;
-      if (dbg) dbg[3] = globaltimer();
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+      if (cur >= target) break;
+      __nanosleep(32);
+      if (globaltimer() - t0 > 4000000000ull) __trap();
+    }
+    if (dbg) {
+      dbg[2] = clock64() - c0;
+      dbg[3] = globaltimer();
     }
   }
   consumers_sync();
@@ -327,8 +197,6 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   constexpr int NV = Pow2Ceil<RR * B>::v;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rchunks = x.r >> 3;
-  long long tg0 = 0;
-  if (x.trace && tid == 0) tg0 = clock64();
   // g is read by every warp of every CTA: fetch it once per CTA (a 148-way instead of a
   // 2368-way hot spot on the same L2 lines), then broadcast through shared memory
   for (int i = tid * 4; i < B * x.r; i += kConsumers * 4)
@@ -350,12 +218,6 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
         for (int e = 0; e < 8; ++e) gr[q][e][b] = 0.f;
       }
     }
-  }
-  if (x.trace && tid == 0) {
-    float sgr = 0.f;
-#pragma unroll
-    for (int q = 0; q < CG; ++q) sgr += gr[q][0][0];
-    x.trace[200] = (unsigned long long)(clock64() - tg0) + (sgr == 1.2345f ? 1 : 0);
   }
   // the two warp groups (warps 0-7, 8-15) take alternate stages, so two stages are in flight
   const int grp = warp >> 3, gw8 = warp & 7;
@@ -506,7 +368,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       // layer's FFN has been fully consumed, and HBM idles through its reduction and the
       // barriers -- pull those stages' rows into L2 so their ring loads hit L2.
       auto prefetch_tail = [&](int li) {
-        if (li != NS || (p.knobs & 2)) return;
+        if (li != NS) return;
         const uint64_t keep = policy_evict_last();
         for (int st = NS; st < st_p1; ++st) {
           const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
@@ -520,7 +382,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
             prefetch_l2(lw.p_w2 + o, (uint32_t)min((size_t)32768, a1 - o), keep);
         }
       };
-      if (!(p.knobs & 16)) {
+      {
         // the small per-layer vectors the consumers read first (b1: every CTA, b2: my slice)
         // would cost an HBM round trip at the start of the layer: pull them into L2 now
         const uint64_t keep = policy_evict_last();
@@ -562,17 +424,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           prefetch_l2(lw.w_up + (size_t)i * row_up, (uint32_t)row_up, keep);
           prefetch_l2(lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, keep);
         }
-      }
-      if (l + 1 < L && (p.knobs & 1)) {   // measured slower (2.533 vs 2.512 ms/step, c4): opt-in
-        // while this layer synchronises and compacts (little HBM traffic), pull the next
-        // layer's predictor rows for this CTA into L2; its ring loads then hit L2
-        const LayerW nx = layer(l + 1);
-        const uint64_t keep = policy_evict_last();
-        for (int k = 0; k < n_p1; ++k)
-          prefetch_l2(nx.p_w1 + (size_t)(c + k * P) * row_dn, (uint32_t)row_dn, keep);
-        const size_t a0 = (size_t)w0 * 32 * rowb2, a1 = (size_t)min(m, w1 * 32) * rowb2;
-        for (size_t o = a0; o < a1; o += 32768)
-          prefetch_l2(nx.p_w2 + o, (uint32_t)min((size_t)32768, a1 - o), keep);
       }
       mbar_wait(ids_ready, l & 1);                 // phase 3: after the ids are published
       const int n_mine = s_k1 - s_k0;
@@ -699,7 +550,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
     }
     if (tr && tid == 0) tr[1] = globaltimer();
-    grid_sync(p.bar, P, tr ? tr + 204 : nullptr, p.knobs & 8);
+    grid_sync(p.bar, P, tr ? tr + 204 : nullptr);
     if (tr && tid == 0) tr[2] = globaltimer();
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
@@ -717,7 +568,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       p.counts[c] = s_count;
       mbar_arrive(p2_done);
     }
-    grid_sync(p.bar, P, tr ? tr + 212 : nullptr, p.knobs & 8);
+    grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
     if (tr && tid == 0) tr[4] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
@@ -931,7 +782,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     ring = it_ffn + n_st;
 
     if (tr && tid == 0) tr[6] = globaltimer();
-    grid_sync(p.bar, P, tr ? tr + 208 : nullptr, p.knobs & 8);
+    grid_sync(p.bar, P, tr ? tr + 208 : nullptr);
     if (tr && tid == 0) tr[7] = globaltimer();
 
     // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
@@ -965,86 +816,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
     }
     if (tr && tid == 0) tr[8] = globaltimer();
-    if (l < L - 1) grid_sync(p.bar, P, tr ? tr + 216 : nullptr, p.knobs & 8);   // the next layer reads all of y
+    if (l < L - 1) grid_sync(p.bar, P, tr ? tr + 216 : nullptr);   // the next layer reads all of y
   }
 }
 
-// ---------------------------------------------------------------------------
-// host side
-// ---------------------------------------------------------------------------
-inline int fused_ch(int d) { return (d / 8 + kGroup - 1) / kGroup; }
-
-template <class Alloc>
-inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc) {
-  w = FusedWork{};
-  w.d = d;
-  w.m = m;
-  w.r = r;
-  w.reglu = reglu;
-  const int ch = fused_ch(d);
-  if (ch > kMaxCH || ch == 5 || ch == 7 || r > 8 * 32 * kMaxCG || d < 8 || r > 16 * num_sms || num_sms > 256)
-    return true;  // unsupported shape: stays disabled (per-step kernels)
-  w.P = num_sms;
-  // stage: >= one neuron (gate|up + down), one P2 word block, >= 32 KB
-  const size_t nb = (size_t)d * (reglu ? 6 : 4);
-  size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, (size_t)32 * r * 2});
-  sb = (sb + 127) / 128 * 128;
-  const size_t budget = 200 * 1024;
-  w.NS = (int)(budget / sb);
-  if (w.NS < 2) return true;
-  w.stage_bytes = (int)sb;
-  // compaction stages the union words, the per-token words and the P counts in one ring slot
-  if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)num_sms * 4 > sb) return true;
-  w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / ((size_t)32 * r * 2)));
-  w.idcap = (m + w.P - 1) / w.P + 2;
-  const int words_all = (m + 31) / 32;
-  w.wcap = (words_all + w.P - 1) / w.P + 1;
-  const size_t extra = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 +
-                       (size_t)w.idcap * 9;
-  w.part_off = (int)(((size_t)w.NS * sb + extra + 15) / 16 * 16);
-  w.pcap = (d + w.P - 1) / w.P + 1;
-  w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * r * 4 + 64;
-  const int words = (m + 31) / 32;
-  if (!alloc((void **)&w.bar, (size_t)(1 + num_sms) * 128 + 128)) return false;
-  if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
-  if (!alloc((void **)&w.ypart, (size_t)w.P * std::min(maxB, kFusedMaxB) * d * 4)) return false;
-  if (!alloc((void **)&w.counts, (size_t)w.P * 4)) return false;
-  if (!alloc((void **)&w.mask, (size_t)maxB * words * 4)) return false;
-  if (!alloc((void **)&w.uni, (size_t)words * 4)) return false;
-  if (!alloc((void **)&w.xbuf, (size_t)std::min(maxB, kFusedMaxB) * d * 4)) return false;
-  if (w.smem > 227 * 1024) return true;
-  w.enabled = true;
-  return true;
-}
-
-inline void fused_init(FusedWork &w, cudaStream_t s) {
-  if (w.enabled) cudaMemsetAsync(w.bar, 0, (size_t)(1 + w.P) * 128 + 128, s);
-}
-
-// neurons per stage (NA template bound and runtime G) and P1 rows per stage
-inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *NA, int *G, int *RP1) {
-  const size_t nb = (size_t)d * 2 * (reglu ? 3 : 2);
-  const int g = (int)(w.stage_bytes / nb);
-  *NA = g >= 2 ? 8 : 1;
-  *G = std::min(*NA, std::max(1, g));
-  const int rp = (int)(w.stage_bytes / ((size_t)d * 2));
-  *RP1 = std::max(1, std::min(*NA == 1 ? 2 : 8, rp));
-}
-
-inline bool fused_supported(const FusedWork &w, int B = 1) {
-  if (!w.enabled || B < 1 || B > kFusedMaxB) return false;
-  const int ch = fused_ch(w.d);
-  if (ch * 8 * B > 64) return false;  // register-resident x / y per group thread
-  int NA, G, RP1;
-  fused_geometry(w, w.d, w.reglu, &NA, &G, &RP1);
-  // the instantiated (CH, NA) combinations (fused_launch)
-  if (ch <= 2) return true;
-  return NA == 1 && (ch == 3 || ch == 4 || (B == 1 && (ch == 6 || ch == 8)));
-}
 
 template <typename T, int B, bool REGLU, int CH, int NA>
-inline cudaError_t fused_launch_t(FusedWork &w, const FusedParams &prm, cudaStream_t s) {
+inline cudaError_t fused_launch_t(const FusedWork &w, const FusedParams &prm, cudaStream_t s) {
   auto kern = k_layer<T, B, REGLU, CH, NA>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, w.smem);
   if (e != cudaSuccess) return e;
@@ -1061,93 +839,20 @@ inline cudaError_t fused_launch_t(FusedWork &w, const FusedParams &prm, cudaStre
   return cudaLaunchKernelEx(&cfg, kern, prm);
 }
 
-// Parameters shared by the single-layer and the stack launch.
-inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
-  FusedParams p{};
-  p.lw0.w_up = (const uint8_t *)a.w_up;
-  p.lw0.w_down = (const uint8_t *)a.w_down;
-  p.lw0.p_w1 = (const uint8_t *)a.p_w1;
-  p.lw0.p_w2 = (const uint8_t *)a.p_w2;
-  p.lw0.b_up = a.b_up;
-  p.lw0.b_down = a.b_down;
-  p.lw0.p_b1 = a.p_b1;
-  p.lw0.p_b2 = a.p_b2;
-  p.lw0.t = a.threshold;
-  p.lw0.hot_ids = a.hot_ids;
-  p.lw0.n_hot = a.n_hot;
-  p.lws = nullptr;
-  p.L = 1;
-  p.x = a.x;
-  p.y = a.y;
-  p.xbuf = w.xbuf;
-  p.d = a.d;
-  p.m = a.m;
-  p.r = a.r;
-  p.words = a.words;
-  p.B = a.B;
-  p.rmsnorm = a.rmsnorm;
-  p.pred_relu = a.pred_relu;
-  p.mask = a.mask_out ? a.mask_out : w.mask;
-  p.uni = w.uni;
-  p.ids_out = a.ids_out;
-  p.n_out = a.n_out;
-  p.g = w.g;
-  p.ypart = w.ypart;
-  p.counts = w.counts;
-  p.bar = w.bar;
-  p.NS = w.NS;
-  p.stage_bytes = w.stage_bytes;
-  p.words_p2 = w.words_p2;
-  p.idcap = w.idcap;
-  p.wcap = w.wcap;
-  p.part_off = w.part_off;
-  p.pcap = w.pcap;
-  p.trace = w.trace;
-  {
-    const char *e = getenv("PI_FUSED_KNOBS");
-    p.knobs = e ? atoi(e) : 0;
-    const char *h = getenv("PI_HOT_CAP");
-    p.hot_cap = h ? atoi(h) : 512;
+// the instantiated (CH, NA) combinations for one (T, B, REGLU); fused_supported() mirrors this list
+template <typename T, int B, bool RG>
+cudaError_t fused_launch_tbr(const FusedWork &w, const FusedParams &p, int CH, int NA, cudaStream_t s) {
+#define PI_FL(CHV, NAV) \
+  if (CH == CHV && NA == NAV) return fused_launch_t<T, B, RG, CHV, NAV>(w, p, s);
+  PI_FL(1, 8) PI_FL(1, 1) PI_FL(2, 8) PI_FL(2, 1) PI_FL(3, 1) PI_FL(4, 1)
+  if (B == 1) {
+    PI_FL(6, 1) PI_FL(8, 1)
   }
-  return p;
-}
-
-template <typename T>
-inline cudaError_t fused_launch_p(FusedWork &w, FusedParams p, bool reglu, int B, cudaStream_t s) {
-  int NA, G, RP1;
-  fused_geometry(w, p.d, reglu, &NA, &G, &RP1);
-  p.G = G;
-  p.rows_p1 = RP1;
-  const int CH = fused_ch(p.d);
-#define PI_FL(NB, RG, CHV, NAV) \
-  if (B == NB && reglu == RG && CH == CHV && NA == NAV) return fused_launch_t<T, NB, RG, CHV, NAV>(w, p, s);
-#define PI_FL_RG(NB, RG)                                                                       \
-  PI_FL(NB, RG, 1, 8) PI_FL(NB, RG, 1, 1) PI_FL(NB, RG, 2, 8) PI_FL(NB, RG, 2, 1) PI_FL(NB, RG, 3, 1) \
-  PI_FL(NB, RG, 4, 1)
-  PI_FL_RG(1, false) PI_FL_RG(1, true) PI_FL_RG(2, false) PI_FL_RG(2, true)
-  PI_FL(1, false, 6, 1) PI_FL(1, true, 6, 1) PI_FL(1, false, 8, 1) PI_FL(1, true, 8, 1)
-#undef PI_FL_RG
 #undef PI_FL
   return cudaErrorNotSupported;
 }
 
-// one layer
-template <typename T>
-inline cudaError_t fused_launch(FusedWork &w, const FusedArgs &a, int /*num_sms*/, cudaStream_t s) {
-  return fused_launch_p<T>(w, fused_params(w, a), a.reglu, a.B, s);
-}
-
-// L chained layers in one launch: a describes layer 0 (shapes, x, y); lws is a device array of
-// the L layers' weights; n_out (optional) receives the L union counts.
-template <typename T>
-inline cudaError_t fused_launch_stack(FusedWork &w, const FusedArgs &a, const LayerW *lws, int L,
-                                      cudaStream_t s) {
-  FusedParams p = fused_params(w, a);
-  p.lws = lws;
-  p.L = L;
-  p.mask = w.mask;
-  p.ids_out = nullptr;
-  return fused_launch_p<T>(w, p, a.reglu, a.B, s);
-}
+#define PI_FUSED_INSTANTIATE(T, B, RG) \
+  template cudaError_t fused_launch_tbr<T, B, RG>(const FusedWork &, const FusedParams &, int, int, cudaStream_t);
 
 }  // namespace pi

@@ -1,0 +1,6 @@
+// k_layer for f16 weights, batch 2, relu (one instantiation unit; see fused.cuh)
+#include "fused.cuh"
+
+namespace pi {
+PI_FUSED_INSTANTIATE(__half, 2, false)
+}  // namespace pi

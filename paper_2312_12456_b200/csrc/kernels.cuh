@@ -6,35 +6,12 @@
 // so results are bitwise reproducible run to run.
 #pragma once
 
-#include "common.cuh"
+#include <algorithm>
+#include <type_traits>
+
+#include "launch.h"
 
 namespace pi {
-
-constexpr float kRmsEps = 1e-6f;  // reading R19
-
-// ---------------------------------------------------------------------------
-// per-token input scale: s_b = rsqrt(mean(x_b^2) + eps)   (PI_FLAG_INPUT_RMSNORM)
-// grid = B blocks, 256 threads.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_rms_scale(const float *__restrict__ x, int d,
-                                                    float *__restrict__ scale) {
-  const int b = blockIdx.x;
-  const float *xb = x + (int64_t)b * d;
-  float s = 0.f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    const float v = xb[j];
-    s = fmaf(v, v, s);
-  }
-  __shared__ float red[8];
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    scale[b] = rsqrtf(t / (float)d + kRmsEps);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // a1: g[b, j] = act_p(s_b * (P1[j] . x_b) + b1[j])
@@ -156,55 +133,6 @@ __global__ void __launch_bounds__(128) k_predict2(const T *__restrict__ p2, cons
     if (lane == 0) mask[(int64_t)b * words + word] = bits;
     if (logits && i < m) logits[(int64_t)b * m + i] = z;
   }
-}
-
-// ---------------------------------------------------------------------------
-// a3: compaction of the union mask into ascending ids (single CTA, 1024 threads).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ mask, int B, int words,
-                                                   int32_t *__restrict__ ids,
-                                                   int32_t *__restrict__ n_active) {
-  __shared__ int wsum[32];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int per = (words + blockDim.x - 1) / blockDim.x;
-  const int w0 = min(words, tid * per), w1 = min(words, w0 + per);
-  int cnt = 0;
-  for (int w = w0; w < w1; ++w) {
-    uint32_t u = 0;
-    for (int b = 0; b < B; ++b) u |= mask[(int64_t)b * words + w];
-    cnt += __popc(u);
-  }
-  // block exclusive scan of cnt
-  int incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int v = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0;
-    int iv = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, iv, o);
-      if (lane >= o) iv += t;
-    }
-    wsum[lane] = iv - v;                  // exclusive warp offsets
-  }
-  __syncthreads();
-  int off = wsum[warp] + incl - cnt;
-  for (int w = w0; w < w1; ++w) {
-    uint32_t u = 0;
-    for (int b = 0; b < B; ++b) u |= mask[(int64_t)b * words + w];
-    while (u) {
-      const int bit = __ffs(u) - 1;
-      ids[off++] = w * 32 + bit;
-      u &= u - 1;
-    }
-  }
-  if (tid == blockDim.x - 1) *n_active = off;
 }
 
 // ---------------------------------------------------------------------------
@@ -347,36 +275,69 @@ __global__ void __launch_bounds__(256) k_down(const T *__restrict__ wdt, const T
 }
 
 // ---------------------------------------------------------------------------
-// create-time repacking (not on the hot path)
+// launchers of the per-step kernels for one weight type (instantiated in steps_inst_<T>.cu)
 // ---------------------------------------------------------------------------
-// dst[k, dst_off + j] = src[nid[k], j] for j < cols  (rows of 16-bit elements)
-__global__ void k_gather_rows(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid,
-                              int rows, int cols, int64_t dst_stride, int dst_off,
-                              uint16_t *__restrict__ dst) {
-  const int k = blockIdx.y;
-  if (k >= rows) return;
-  const int64_t sr = nid ? nid[k] : k;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
-    dst[(int64_t)k * dst_stride + dst_off + j] = src[sr * cols + j];
+template <class F>
+static cudaError_t dispatch_batch(int B, F &&f) {
+  switch (B) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+  }
+  return cudaErrorInvalidValue;
 }
 
-// dst[k, j] = src[j, nid[k]]: transpose-gather of nn.Linear W_down [d, m_total] into [m_local, d].
-__global__ void k_transpose_gather(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid,
-                                   int d, int m_total, int m_local, uint16_t *__restrict__ dst) {
-  __shared__ uint16_t tileb[32][33];
-  const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
-  for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
-    const int j = j0 + jj, k = k0 + threadIdx.x;
-    if (j < d && k < m_local) {
-      const int64_t col = nid ? nid[k] : k;
-      tileb[jj][threadIdx.x] = src[(int64_t)j * m_total + col];
-    }
-  }
-  __syncthreads();
-  for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
-    const int k = k0 + kk, j = j0 + threadIdx.x;
-    if (k < m_local && j < d) dst[(int64_t)k * d + j] = tileb[threadIdx.x][kk];
-  }
+template <typename T>
+cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float *scale, uint32_t *mask,
+                          float *logits, cudaStream_t s) {
+  return dispatch_batch(B, [&](auto bb) {
+    constexpr int NB = decltype(bb)::value;
+    const int g1 = (a.r + 1) / 2;
+    if (a.pred_relu)
+      k_predict1<T, NB, true><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g);
+    else
+      k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)(NB * a.r + 4 * NB * 32) * 4;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_predict2<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_predict2<T, NB><<<(a.words + 3) / 4, 128, smem, s>>>((const T *)a.p_w2, (const T *)a.p_b2, a.g, a.t, a.m,
+                                                           a.r, a.words, mask, logits);
+    return cudaGetLastError();
+  });
 }
+
+template <typename T>
+cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *scale, const int32_t *ids,
+                      const int32_t *n_active, const uint32_t *mask, float *y, cudaStream_t s) {
+  return dispatch_batch(B, [&](auto bb) {
+    constexpr int NB = decltype(bb)::value;
+    const int gup = std::max(1, std::min((a.m + 7) / 8, a.num_sms * 8));
+    if (a.reglu)
+      k_up<T, NB, true><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
+                                            a.words, a.d, a.h, a.m);
+    else
+      k_up<T, NB, false><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
+                                             a.words, a.d, a.h, a.m);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)8 * NB * 256 * 4;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k_down<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_down<T, NB><<<a.tiles * a.S, 256, smem, s>>>((const T *)a.w_down, (const T *)a.b_down, a.h, a.m, ids,
+                                                    n_active, a.d, a.S, a.tiles, a.partial, a.tickets, y);
+    return cudaGetLastError();
+  });
+}
+
+#define PI_STEPS_INSTANTIATE(T)                                                                              \
+  template cudaError_t steps_predict<T>(const StepArgs &, const float *, int, const float *, uint32_t *, float *, \
+                                        cudaStream_t);                                                        \
+  template cudaError_t steps_ffn<T>(const StepArgs &, const float *, int, const float *, const int32_t *,         \
+                                    const int32_t *, const uint32_t *, float *, cudaStream_t);
 
 }  // namespace pi

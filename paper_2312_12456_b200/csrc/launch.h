@@ -1,0 +1,38 @@
+// launch.h -- host-side entry points into libpi's kernels, one declaration per instantiation
+// unit, so the ABI layer (pi_api.cu) and the kernel units compile independently and in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace pi {
+
+// operands of the per-step kernels (library-owned device pointers of one layer handle)
+struct StepArgs {
+  const void *p_w1, *p_b1, *p_w2, *p_b2, *w_up, *b_up, *w_down, *b_down;
+  float *g, *h, *partial;
+  unsigned *tickets;
+  int d, m, r, words, S, tiles, num_sms;
+  float t;
+  bool pred_relu, reglu;
+};
+
+// kernels.cuh, instantiated per weight type in steps_inst_<T>.cu
+template <typename T>
+cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float *scale, uint32_t *mask,
+                          float *logits, cudaStream_t s);
+template <typename T>
+cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *scale, const int32_t *ids,
+                      const int32_t *n_active, const uint32_t *mask, float *y, cudaStream_t s);
+
+// misc.cu
+cudaError_t launch_rms_scale(const float *x, int B, int d, float *scale, cudaStream_t s);
+cudaError_t launch_compact(const uint32_t *mask, int B, int words, int32_t *ids, int32_t *n_active, cudaStream_t s);
+cudaError_t launch_gather_rows(const void *src, const int32_t *nid, int rows, int cols, int64_t dst_stride,
+                               int dst_off, void *dst, cudaStream_t s);
+cudaError_t launch_transpose_gather(const void *src, const int32_t *nid, int d, int m_total, int m_local,
+                                    void *dst, cudaStream_t s);
+
+}  // namespace pi

@@ -1,0 +1,140 @@
+// misc.cu -- libpi's non-templated kernels: the RMS input scale, the single-CTA compaction used
+// by pi_compact and the per-step path, and the create-time repacking kernels.
+#include "launch.h"
+
+namespace pi {
+
+constexpr float kRmsEps = 1e-6f;  // reading R19
+
+// ---------------------------------------------------------------------------
+// per-token input scale: s_b = rsqrt(mean(x_b^2) + eps)   (PI_FLAG_INPUT_RMSNORM)
+// grid = B blocks, 256 threads.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_rms_scale(const float *__restrict__ x, int d,
+                                                    float *__restrict__ scale) {
+  const int b = blockIdx.x;
+  const float *xb = x + (int64_t)b * d;
+  float s = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float v = xb[j];
+    s = fmaf(v, v, s);
+  }
+  __shared__ float red[8];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    scale[b] = rsqrtf(t / (float)d + kRmsEps);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// a3: compaction of the union mask into ascending ids (single CTA, 1024 threads).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_compact(const uint32_t *__restrict__ mask, int B, int words,
+                                                   int32_t *__restrict__ ids,
+                                                   int32_t *__restrict__ n_active) {
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (words + blockDim.x - 1) / blockDim.x;
+  const int w0 = min(words, tid * per), w1 = min(words, w0 + per);
+  int cnt = 0;
+  for (int w = w0; w < w1; ++w) {
+    uint32_t u = 0;
+    for (int b = 0; b < B; ++b) u |= mask[(int64_t)b * words + w];
+    cnt += __popc(u);
+  }
+  // block exclusive scan of cnt
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = (lane < (int)(blockDim.x >> 5)) ? wsum[lane] : 0;
+    int iv = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, iv, o);
+      if (lane >= o) iv += t;
+    }
+    wsum[lane] = iv - v;                  // exclusive warp offsets
+  }
+  __syncthreads();
+  int off = wsum[warp] + incl - cnt;
+  for (int w = w0; w < w1; ++w) {
+    uint32_t u = 0;
+    for (int b = 0; b < B; ++b) u |= mask[(int64_t)b * words + w];
+    while (u) {
+      const int bit = __ffs(u) - 1;
+      ids[off++] = w * 32 + bit;
+      u &= u - 1;
+    }
+  }
+  if (tid == blockDim.x - 1) *n_active = off;
+}
+
+// ---------------------------------------------------------------------------
+// create-time repacking (not on the hot path)
+// ---------------------------------------------------------------------------
+// dst[k, dst_off + j] = src[nid[k], j] for j < cols  (rows of 16-bit elements)
+__global__ void k_gather_rows(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid,
+                              int rows, int cols, int64_t dst_stride, int dst_off,
+                              uint16_t *__restrict__ dst) {
+  for (int k = blockIdx.y; k < rows; k += gridDim.y) {
+    const int64_t sr = nid ? nid[k] : k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+      dst[(int64_t)k * dst_stride + dst_off + j] = src[sr * cols + j];
+  }
+}
+
+// dst[k, j] = src[j, nid[k]]: transpose-gather of nn.Linear W_down [d, m_total] into [m_local, d].
+__global__ void k_transpose_gather(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid,
+                                   int d, int m_total, int m_local, uint16_t *__restrict__ dst) {
+  __shared__ uint16_t tileb[32][33];
+  const int k0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+    const int j = j0 + jj, k = k0 + threadIdx.x;
+    if (j < d && k < m_local) {
+      const int64_t col = nid ? nid[k] : k;
+      tileb[jj][threadIdx.x] = src[(int64_t)j * m_total + col];
+    }
+  }
+  __syncthreads();
+  for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
+    const int k = k0 + kk, j = j0 + threadIdx.x;
+    if (k < m_local && j < d) dst[(int64_t)k * d + j] = tileb[threadIdx.x][kk];
+  }
+}
+
+cudaError_t launch_rms_scale(const float *x, int B, int d, float *scale, cudaStream_t s) {
+  k_rms_scale<<<B, 256, 0, s>>>(x, d, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const uint32_t *mask, int B, int words, int32_t *ids, int32_t *n_active, cudaStream_t s) {
+  k_compact<<<1, 1024, 0, s>>>(mask, B, words, ids, n_active);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_rows(const void *src, const int32_t *nid, int rows, int cols, int64_t dst_stride,
+                               int dst_off, void *dst, cudaStream_t s) {
+  dim3 grid((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64, rows < 65535 ? rows : 65535);
+  k_gather_rows<<<grid, 256, 0, s>>>((const uint16_t *)src, nid, rows, cols, dst_stride, dst_off, (uint16_t *)dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_gather(const void *src, const int32_t *nid, int d, int m_total, int m_local,
+                                    void *dst, cudaStream_t s) {
+  dim3 grid((m_local + 31) / 32, (d + 31) / 32), block(32, 8);
+  if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+  k_transpose_gather<<<grid, block, 0, s>>>((const uint16_t *)src, nid, d, m_total, m_local, (uint16_t *)dst);
+  return cudaGetLastError();
+}
+
+}  // namespace pi

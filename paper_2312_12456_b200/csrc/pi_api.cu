@@ -2,6 +2,7 @@
 // and dispatch of the sm_100a kernels.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -11,8 +12,8 @@
 #include <vector>
 
 #include "../../include/pi.h"
-#include "fused.cuh"
-#include "kernels.cuh"
+#include "fused_host.h"
+#include "launch.h"
 
 using namespace pi;
 
@@ -50,12 +51,6 @@ pi_status pi_set_error(pi_status st, const char *msg) {
     if (s_ != PI_OK) return s_;     \
   } while (0)
 
-static pi_status check_launch(const char *what) {
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(PI_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
-  return PI_OK;
-}
-
 // ---------------------------------------------------------------------------
 // the handle
 // ---------------------------------------------------------------------------
@@ -85,8 +80,8 @@ struct pi_layer {
   int32_t *n_active = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;  // [max_batch, d] each (stack ping-pong)
   float *hx = nullptr, *hy = nullptr;      // [max_batch, d] each (host-buffer entry points)
-  int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons
-  int n_hot = 0;
+  int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons, hottest first
+  int n_hot = 0, hot_cap = 0;
   FusedWork fw{};             // fused-kernel workspace
   int tiles = 0, S = 0;
   int64_t weight_bytes = 0, ws_bytes = 0;
@@ -120,21 +115,6 @@ template <typename T>
 struct Tag {
   using type = T;
 };
-
-template <class F>
-static pi_status dispatch_b(int B, F &&f) {
-  switch (B) {
-    case 1: return f(IC<1>{});
-    case 2: return f(IC<2>{});
-    case 3: return f(IC<3>{});
-    case 4: return f(IC<4>{});
-    case 5: return f(IC<5>{});
-    case 6: return f(IC<6>{});
-    case 7: return f(IC<7>{});
-    case 8: return f(IC<8>{});
-  }
-  return fail(PI_ERR_INVALID_ARGUMENT, "batch %d out of range 1..%d", B, PI_MAX_BATCH);
-}
 
 template <class F>
 static pi_status dispatch_t(pi_dtype dt, F &&f) {
@@ -270,6 +250,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
 #undef ALLOC
 
   cudaStream_t s = (cudaStream_t)stream;
+  L->hot_cap = D->hot_cap > 0 ? D->hot_cap : PI_DEFAULT_HOT_CAP;
   if (D->neuron_freq) {
     std::vector<int32_t> hot;
     for (int k = 0; k < ml; ++k) {
@@ -277,6 +258,9 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
       const float f = D->neuron_freq[gid];
       if (std::isfinite(f) && f >= D->hot_freq) hot.push_back(k);
     }
+    // hottest first (ties: ascending id), so the kernel's per-layer cap keeps the most frequent
+    auto freq_of = [&](int k) { return D->neuron_freq[D->neuron_ids ? D->neuron_ids[k] : k]; };
+    std::stable_sort(hot.begin(), hot.end(), [&](int a, int b) { return freq_of(a) > freq_of(b); });
     if (!hot.empty()) {
       st = dev_alloc(L, (void **)&L->hot_ids, hot.size() * 4, false);
       if (st != PI_OK) return cleanup(st);
@@ -294,10 +278,10 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
       return cleanup(fail(PI_ERR_CUDA, "layer %d: neuron table copy", lid));
     }
   }
+  cudaError_t ge = cudaSuccess;
   auto gather = [&](const void *src, void *dst, int cols, int64_t dst_stride, int dst_off) {
-    dim3 grid((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64, ml);
-    k_gather_rows<<<grid, 256, 0, s>>>((const uint16_t *)src, d_nid, ml, cols, dst_stride, dst_off,
-                                       (uint16_t *)dst);
+    const cudaError_t e = launch_gather_rows(src, d_nid, ml, cols, dst_stride, dst_off, dst, s);
+    if (ge == cudaSuccess) ge = e;
   };
   if (reglu) {
     gather(D->w_gate, L->w_up, d, 2 * (int64_t)d, 0);
@@ -309,9 +293,8 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   if (D->b_up) gather(D->b_up, L->b_up, 1, 1, 0);
   if (D->p_b2) gather(D->p_b2, L->p_b2, 1, 1, 0);
   {
-    dim3 grid((ml + 31) / 32, (d + 31) / 32), block(32, 8);
-    k_transpose_gather<<<grid, block, 0, s>>>((const uint16_t *)D->w_down, d_nid, d, mt, ml,
-                                              (uint16_t *)L->w_down);
+    const cudaError_t e = launch_transpose_gather(D->w_down, d_nid, d, mt, ml, L->w_down, s);
+    if (ge == cudaSuccess) ge = e;
   }
   cudaMemcpyAsync(L->p_w1, D->p_w1, (size_t)r * d * e, cudaMemcpyDeviceToDevice, s);
   if (D->p_b1) cudaMemcpyAsync(L->p_b1, D->p_b1, (size_t)r * e, cudaMemcpyDeviceToDevice, s);
@@ -320,6 +303,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   cudaMemsetAsync(L->n_active, 0, 16, s);
   fused_init(L->fw, s);
   cudaError_t ce = cudaGetLastError();
+  if (ce == cudaSuccess) ce = ge;
   if (d_nid) {
     // the table must outlive the async gathers (create is not on the hot path)
     cudaStreamSynchronize(s);
@@ -385,7 +369,7 @@ extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, 
     h[l].p_b2 = Ll->p_b2;
     h[l].t = Ll->threshold;
     h[l].hot_ids = Ll->hot_ids;
-    h[l].n_hot = Ll->n_hot;
+    h[l].n_hot = std::min(Ll->n_hot, Ll->hot_cap);
   }
   if (cudaMalloc(&S->lws, sizeof(LayerW) * n_layers) != cudaSuccess) {
     delete S;
@@ -420,6 +404,7 @@ static pi_status stack_run_dev(pi_stack *S, const float *x, int B, float *y, int
       a.threshold = L0->threshold; a.rmsnorm = (L0->flags & PI_FLAG_INPUT_RMSNORM) != 0;
       a.pred_relu = L0->pred_act == PI_PRED_RELU; a.reglu = L0->act == PI_ACT_REGLU;
       a.n_out = n_out;
+      a.hot_cap = L0->hot_cap;
       cudaError_t e = fused_launch_stack<T>(L0->fw, a, S->lws, n, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "stack: fused launch: %s", cudaGetErrorString(e));
       return PI_OK;
@@ -493,59 +478,40 @@ static pi_status check_common(const pi_layer *L, int B) {
 // scale pointer for the RMS flag (launches the scale kernel) or NULL
 static const float *launch_scale(pi_layer *L, const float *x, int B, cudaStream_t s) {
   if (!(L->flags & PI_FLAG_INPUT_RMSNORM)) return nullptr;
-  k_rms_scale<<<B, 256, 0, s>>>(x, L->d, L->scale);
+  launch_rms_scale(x, B, L->d, L->scale, s);
   return L->scale;
+}
+
+static StepArgs step_args(const pi_layer *L) {
+  StepArgs a{};
+  a.p_w1 = L->p_w1; a.p_b1 = L->p_b1; a.p_w2 = L->p_w2; a.p_b2 = L->p_b2;
+  a.w_up = L->w_up; a.b_up = L->b_up; a.w_down = L->w_down; a.b_down = L->b_down;
+  a.g = L->g; a.h = L->h; a.partial = L->partial; a.tickets = L->tickets;
+  a.d = L->d; a.m = L->m_local; a.r = L->r; a.words = L->words; a.S = L->S; a.tiles = L->tiles;
+  a.num_sms = L->num_sms; a.t = L->threshold;
+  a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
+  return a;
+}
+
+static pi_status cuda_status(cudaError_t e, const pi_layer *L, const char *what) {
+  if (e == cudaSuccess) return PI_OK;
+  return fail(PI_ERR_CUDA, "layer %d: %s launch: %s", L->layer_id, what, cudaGetErrorString(e));
 }
 
 static pi_status run_predict(pi_layer *L, const float *x, int B, const float *scale, uint32_t *mask,
                              float *logits, cudaStream_t s) {
-  return dispatch_t(L->dtype, [&](auto tt) {
-    using T = typename decltype(tt)::type;
-    return dispatch_b(B, [&](auto bb) {
-      constexpr int NB = decltype(bb)::value;
-      const int g1 = (L->r + 1) / 2;
-      if (L->pred_act == PI_PRED_RELU)
-        k_predict1<T, NB, true><<<g1, 256, 0, s>>>((const T *)L->p_w1, (const T *)L->p_b1, x, scale, L->r,
-                                                   L->d, L->g);
-      else
-        k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)L->p_w1, (const T *)L->p_b1, x, scale, L->r,
-                                                    L->d, L->g);
-      PI_TRY(check_launch("predict1"));
-      const size_t smem = (size_t)(NB * L->r + 4 * NB * 32) * 4;
-      if (smem > 48 * 1024) {
-        cudaFuncSetAttribute(k_predict2<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      }
-      k_predict2<T, NB><<<(L->words + 3) / 4, 128, smem, s>>>((const T *)L->p_w2, (const T *)L->p_b2, L->g,
-                                                               L->threshold, L->m_local, L->r, L->words,
-                                                               mask, logits);
-      return check_launch("predict2");
-    });
-  });
+  const StepArgs a = step_args(L);
+  const cudaError_t e = L->dtype == PI_DT_F16 ? steps_predict<__half>(a, x, B, scale, mask, logits, s)
+                                              : steps_predict<__nv_bfloat16>(a, x, B, scale, mask, logits, s);
+  return cuda_status(e, L, "predict");
 }
 
 static pi_status run_ffn(pi_layer *L, const float *x, int B, const float *scale, const int32_t *ids,
                          const int32_t *n_active, const uint32_t *mask, float *y, cudaStream_t s) {
-  return dispatch_t(L->dtype, [&](auto tt) {
-    using T = typename decltype(tt)::type;
-    return dispatch_b(B, [&](auto bb) {
-      constexpr int NB = decltype(bb)::value;
-      const int gup = std::max(1, std::min((L->m_local + 7) / 8, L->num_sms * 8));
-      if (L->act == PI_ACT_REGLU)
-        k_up<T, NB, true><<<gup, 256, 0, s>>>((const T *)L->w_up, (const T *)L->b_up, x, scale, ids, n_active,
-                                              mask, L->words, L->d, L->h, L->m_local);
-      else
-        k_up<T, NB, false><<<gup, 256, 0, s>>>((const T *)L->w_up, (const T *)L->b_up, x, scale, ids,
-                                               n_active, mask, L->words, L->d, L->h, L->m_local);
-      PI_TRY(check_launch("up"));
-      const size_t smem = (size_t)8 * NB * 256 * 4;
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(k_down<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_down<T, NB><<<L->tiles * L->S, 256, smem, s>>>((const T *)L->w_down, (const T *)L->b_down, L->h,
-                                                       L->m_local, ids, n_active, L->d, L->S, L->tiles,
-                                                       L->partial, L->tickets, y);
-      return check_launch("down");
-    });
-  });
+  const StepArgs a = step_args(L);
+  const cudaError_t e = L->dtype == PI_DT_F16 ? steps_ffn<__half>(a, x, B, scale, ids, n_active, mask, y, s)
+                                              : steps_ffn<__nv_bfloat16>(a, x, B, scale, ids, n_active, mask, y, s);
+  return cuda_status(e, L, "sparse ffn");
 }
 
 extern "C" pi_status pi_predict(pi_layer *L, const float *x, int32_t B, uint32_t *mask, float *logits,
@@ -565,8 +531,7 @@ extern "C" pi_status pi_compact(pi_layer *L, const uint32_t *mask, int32_t B, in
   PI_TRY(check_common(L, B));
   if (!mask || !ids || !n_active)
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: mask, ids, n_active are required", L->layer_id);
-  k_compact<<<1, 1024, 0, (cudaStream_t)stream>>>(mask, B, L->words, ids, n_active);
-  return check_launch("compact");
+  return cuda_status(launch_compact(mask, B, L->words, ids, n_active, (cudaStream_t)stream), L, "compact");
 }
 
 extern "C" pi_status pi_sparse_ffn(pi_layer *L, const float *x, int32_t B, const int32_t *ids,
@@ -597,7 +562,7 @@ static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint3
       a.threshold = L->threshold; a.rmsnorm = (L->flags & PI_FLAG_INPUT_RMSNORM) != 0;
       a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
       a.mask_out = mask_out; a.ids_out = ids_out; a.n_out = n_out;
-      a.hot_ids = L->hot_ids; a.n_hot = L->n_hot;
+      a.hot_ids = L->hot_ids; a.n_hot = L->n_hot; a.hot_cap = L->hot_cap;
       cudaError_t e = fused_launch<T>(L->fw, a, L->num_sms, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "layer %d: fused launch: %s", L->layer_id, cudaGetErrorString(e));
       return PI_OK;
@@ -608,8 +573,7 @@ static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint3
   int32_t *n = n_out ? n_out : L->n_active;
   const float *scale = launch_scale(L, x, B, s);
   PI_TRY(run_predict(L, x, B, scale, mask, nullptr, s));
-  k_compact<<<1, 1024, 0, s>>>(mask, B, L->words, ids, n);
-  PI_TRY(check_launch("compact"));
+  PI_TRY(cuda_status(launch_compact(mask, B, L->words, ids, n, s), L, "compact"));
   return run_ffn(L, x, B, scale, ids, n, mask, y, s);
 }
 

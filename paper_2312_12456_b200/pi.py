@@ -55,7 +55,7 @@ class LayerDesc(ctypes.Structure):
                 ("p_b1", ctypes.c_void_p), ("p_w2", ctypes.c_void_p), ("p_b2", ctypes.c_void_p),
                 ("logit_threshold", ctypes.c_float), ("max_batch", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("neuron_freq", ctypes.POINTER(ctypes.c_float)),
-                ("hot_freq", ctypes.c_float)]
+                ("hot_freq", ctypes.c_float), ("hot_cap", ctypes.c_int32)]
 
 
 class LayerInfo(ctypes.Structure):
@@ -138,7 +138,8 @@ class Layer:
 
     def __init__(self, w, neuron_ids: Optional[Sequence[int]] = None, max_batch: int = 1, flags: int = 0,
                  layer_id: int = 0, threshold: Optional[float] = None, pred_act: Optional[str] = None,
-                 own_b_down: bool = True, stream=None, neuron_freq=None, hot_freq: float = 0.9):
+                 own_b_down: bool = True, stream=None, neuron_freq=None, hot_freq: float = 0.9,
+                 hot_cap: int = 0):
         self.handle = None
         dt = w.w_up.dtype
         if dt not in _DT:
@@ -163,7 +164,8 @@ class Layer:
                          PI_PRED_RELU if pa == "relu" else PI_PRED_LINEAR,
                          _ptr(w.w_up), _ptr(w.w_gate), _ptr(w.w_down), _ptr(w.b_up),
                          _ptr(w.b_down) if own_b_down else None, _ptr(w.p_w1), _ptr(w.p_b1), _ptr(w.p_w2),
-                         _ptr(w.p_b2), float(thr), int(max_batch), int(flags), freq_p, float(hot_freq))
+                         _ptr(w.p_b2), float(thr), int(max_batch), int(flags), freq_p, float(hot_freq),
+                         int(hot_cap))
         h = ctypes.c_void_p()
         s = _stream(stream)
         _check(_lib.pi_layer_create(ctypes.byref(desc), s, ctypes.byref(h)))
@@ -209,7 +211,10 @@ class Layer:
                                           _stream(stream)))
 
     def set_trace(self, buf: Optional[torch.Tensor]):
-        """Phase timestamps of the fused kernel into buf (int64 [num_sms * 128]); None = off."""
+        """Phase timestamps of the fused kernel into buf (int64 [num_sms * 256], include/pi.h);
+        None = off."""
+        if buf is not None and (buf.dtype != torch.int64 or buf.numel() < self.info.num_sms * 256):
+            raise ValueError(f"trace buffer must be int64 with >= {self.info.num_sms * 256} elements")
         _check(_lib.pi_layer_set_trace(self.handle, _ptr(buf)))
 
     # --- buffers sized for this layer ---

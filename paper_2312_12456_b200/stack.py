@@ -55,19 +55,49 @@ class Stack:
         return len(self.layers)
 
     def step(self, x: torch.Tensor, y: torch.Tensor, n_out: Optional[torch.Tensor] = None,
-             bufs: Optional[List[torch.Tensor]] = None):
-        """One decode step for B tokens through every layer.  World size 1: one pi_stack_forward
-        call.  World size > 1: per layer pi_layer_forward on the local shard, then all-reduce."""
+             bufs: Optional[List[torch.Tensor]] = None, record: Optional[list] = None):
+        """One decode step for B tokens through every layer.  World size 1: one pi_stack_run
+        call (one persistent launch).  World size > 1: per layer pi_layer_forward on the local
+        shard (partial output, b_down on rank 0 only), then all-reduce(sum) of the partials
+        (the paper's merge).  ``record`` (tests): each layer's merged output is
+        appended to it (world > 1)."""
         if self.world == 1:
             self.stack.run(x, y, n_out)
             return y
+        if bufs is None:
+            bufs = self._bufs(x)
         cur = x
         for l, L in enumerate(self.layers):
             dst = y if l == len(self.layers) - 1 else bufs[l & 1]
             L.forward(cur, dst, None, None, None if n_out is None else n_out[l:l + 1])
             dist.all_reduce(dst, op=dist.ReduceOp.SUM, group=self.group)
+            if record is not None:
+                record.append(dst.clone())
             cur = dst
         return y
+
+    def _bufs(self, x: torch.Tensor) -> List[torch.Tensor]:
+        key = (x.shape[0], x.device)
+        if getattr(self, "_buf_key", None) != key:
+            self._buf = [torch.empty(x.shape[0], self.d, device=x.device) for _ in range(2)]
+            self._buf_key = key
+        return self._buf
+
+    def capture(self, x: torch.Tensor, y: torch.Tensor, n_out: Optional[torch.Tensor] = None):
+        """Capture one decode step (static x -> y; every layer's kernel and, for world > 1, its
+        NCCL all-reduce) into a CUDA graph; returns the graph -- replay() runs the step with one
+        launch from the host.  The caller writes each token into x before replaying."""
+        bufs = self._bufs(x)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):           # warm-up on a side stream (NCCL communicator init)
+            self.step(x, y, n_out, bufs)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(x, y, n_out, bufs)
+        return g
 
     def close(self):
         if self.stack is not None:
@@ -88,7 +118,8 @@ def shard_ids(p: np.ndarray, world: int, rank: int, granule: int = 64) -> Option
 
 def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, world: int = 1, seed: int = 0,
                 device="cuda", max_batch: int = 1, mean_act: float = 0.10, group=None,
-                keep_weights: bool = False, dims: Optional[dict] = None, hot_freq: Optional[float] = None):
+                keep_weights: bool = False, dims: Optional[dict] = None, hot_freq: Optional[float] = None,
+                hot_cap: int = 0):
     """Generate the config's layers (random init, seeded) and create this rank's handles.
 
     Returns (Stack, weights-or-None).  With keep_weights the generator tensors stay alive
@@ -105,7 +136,8 @@ def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, 
         # the planted activity profile plays the paper's profiler frequencies f_i (Eq. 1)
         freq = None if hot_freq is None else w.p
         layers.append(pi.Layer(w, neuron_ids=nid, max_batch=max_batch, flags=flags, layer_id=l, own_b_down=own,
-                               neuron_freq=freq, hot_freq=hot_freq if hot_freq is not None else 2.0))
+                               neuron_freq=freq, hot_freq=hot_freq if hot_freq is not None else 2.0,
+                               hot_cap=hot_cap))
         m_local = w.m if nid is None else len(nid)
         metas.append(LayerMeta(w.d, m_local, w.r, w.act == "reglu", w.b_up is not None,
                                own and w.b_down is not None, w.p_b1 is not None, w.p_b2 is not None))

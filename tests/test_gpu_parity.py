@@ -476,3 +476,77 @@ def test_hot_neuron_prefetch_changes_nothing(env):
         outs.append(y.clone())
         S.close()
     assert torch.equal(outs[0], outs[1])
+
+
+def test_cuda_graph_capture_replay(env):
+    """pi_stack_run, pi_layer_forward (fused) and the per-step path (PI_FLAG_MULTI_KERNEL) are
+    stream-ordered and capturable: a captured CUDA graph replays to the eager result bit for bit,
+    including for a new token written into the captured input buffer (include/pi.h)."""
+    gen, pi = env
+    from paper_2312_12456_b200.stack import build_stack
+    cfg = gen.CONFIGS["c4"]
+    dims = {"d": 2048, "m": 4096, "r": 64}
+    st, _ = build_stack(cfg, n_layers=3, seed=3, device="cuda", max_batch=2, dims=dims)
+    x = gen.tokens(2, 2048, seed=1, device="cuda")
+    y = torch.empty_like(x)
+    g = st.capture(x, y)
+    for tok in range(3):
+        x.copy_(gen.tokens(2, 2048, seed=1, step=tok, device="cuda"))
+        y_eager = torch.empty_like(y)
+        st.step(x, y_eager)
+        y.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y, y_eager), tok
+    st.close()
+    w = gen.make_layer(cfg, seed=4, device="cuda", **dims)
+    for flags in (0, pi.PI_FLAG_MULTI_KERNEL):
+        L = pi.Layer(w, max_batch=2, flags=flags)
+        x = gen.tokens(2, 2048, seed=2, device="cuda")
+        y = torch.empty_like(x)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            L.forward(x, y)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        ref = y.clone()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            L.forward(x, y)
+        y.fill_(float("nan"))
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref), flags
+        L.close()
+
+
+def test_full_size_c4_stack_bench_configuration(env):
+    """The bench's exact launch configuration at full c4 size: 4 layers of d 8192, m 32768, r 512 with
+    the hot-neuron L2 prefetch on (planted profile as neuron_freq, hot_freq 0.99, cap 512).  Equal bit
+    for bit to the same stack with the prefetch off, and every layer matches the oracle on its own
+    GPU input (R20)."""
+    gen, pi = env
+    from paper_2312_12456_b200.stack import build_stack
+    cfg = gen.CONFIGS["c4"]
+    x = gen.tokens(1, cfg.d, seed=7, device="cuda")
+    outs = []
+    for hot in (0.99, None):
+        st, kept = build_stack(cfg, n_layers=4, seed=0, device="cuda", max_batch=1, keep_weights=(hot is not None),
+                               hot_freq=hot, hot_cap=512)
+        y = torch.empty_like(x)
+        st.step(x, y)
+        torch.cuda.synchronize()
+        outs.append(y.clone())
+        if hot is not None:
+            assert st.layers[0].info.launches_per_forward == 1
+            cur = x
+            for l, (w, _) in enumerate(kept):
+                yl, gm, ids, nl = run_forward(pi, st.layers[l], cur)
+                oracle_check(w, cur, yl, gm, ids, norm=cfg.rmsnorm)
+                cur = torch.from_numpy(yl).cuda()
+            assert torch.equal(cur, y)
+            del kept
+        st.close()
+        torch.cuda.empty_cache()
+    assert torch.equal(outs[0], outs[1])

@@ -128,3 +128,59 @@ def test_exhaustive_cover_small():
             continue
         owner, ids, off = OP.partition([float(i) for i in range(m)], G, 1)
         OP.check_partition(owner, ids, off, m, G, 1)
+
+
+# --- negative pins: check_partition (O8) must reject every kind of invalid placement ---------
+# A valid base placement: m = 8, G = 2, granule 2 (shard 0 = {0, 1, 4, 5}, shard 1 = {2, 3, 6, 7}).
+_OWNER = [0, 0, 1, 1, 0, 0, 1, 1]
+_IDS = [0, 1, 4, 5, 2, 3, 6, 7]
+_OFF = [0, 4, 8]
+
+
+def _bad(owner, ids, off, m=8, G=2, granule=2):
+    with pytest.raises(AssertionError):
+        OP.check_partition(owner, ids, off, m, G, granule)
+
+
+def test_check_partition_accepts_the_base_case():
+    OP.check_partition(_OWNER, _IDS, _OFF, 8, 2, 2)
+
+
+def test_check_partition_rejects_overlap():
+    # neuron 4 listed on both shards, neuron 2 on none (Eq. 3: exactly one unit)
+    _bad(_OWNER, [0, 1, 4, 5, 3, 4, 6, 7], _OFF)
+
+
+def test_check_partition_rejects_gap():
+    # neuron 7 missing; id 8 out of range instead (exact cover of [0, m))
+    _bad(_OWNER, [0, 1, 4, 5, 2, 3, 6, 8], _OFF)
+
+
+def test_check_partition_rejects_unequal_counts():
+    # shard 0 gets 3 neurons, shard 1 gets 5 (Eq. 6 with equal capacities)
+    _bad([0, 0, 1, 1, 0, 1, 1, 1], [0, 1, 4, 2, 3, 5, 6, 7], [0, 3, 8])
+
+
+def test_check_partition_rejects_counts_not_multiple_of_granule():
+    # equal counts of 4 are fine for granule 2 but not for granule 8 (P:809 runs)
+    _bad(_OWNER, _IDS, _OFF, granule=8)
+
+
+def test_check_partition_rejects_non_ascending_shard():
+    _bad(_OWNER, [0, 4, 1, 5, 2, 3, 6, 7], _OFF)
+
+
+def test_check_partition_rejects_owner_mismatch():
+    # shard lists are a valid cover, but owner[] disagrees for neuron 6
+    _bad([0, 0, 1, 1, 0, 0, 0, 1], _IDS, _OFF)
+
+
+def test_check_partition_rejects_bad_offsets():
+    _bad(_OWNER, _IDS, [1, 4, 8])
+    _bad(_OWNER, _IDS, [0, 4, 7])
+    _bad(_OWNER, _IDS, [0, 8])                       # wrong length for G = 2
+
+
+def test_check_partition_rejects_wrong_lengths():
+    _bad(_OWNER[:-1], _IDS, _OFF)
+    _bad(_OWNER, _IDS[:-1], _OFF)
