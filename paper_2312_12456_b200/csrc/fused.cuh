@@ -171,93 +171,116 @@ __device__ __forceinline__ float up_total(const float *red, int i) {
 }
 
 // ---------------------------------------------------------------------------
-// phase 2: z = P2 g + b2 ; bit = z > t ; ballot.  All 16 consumer warps share each ring stage
-// (a block of mask words): warp w takes rows {R (w + 16 k) .. +R-1} (R = 2 / B), each lane owns
-// CG 16-byte chunks of r (g for those chunks in registers), a transpose reduction leaves each
-// (token, row) logit in one lane, logits go to zbuf, and after a consumer barrier one warp per
-// mask word ballots, writes the per-token words, the union word and its popcount.
+// phase 2: z = P2 g + b2 ; bit = z > t ; ballot -- on the tensor cores.
+// g (fp32, every CTA reads all of it) is fetched once per CTA into shared memory and turned into
+// the B fragments of mma.m16n8k16: three 16-bit splits per value, power-of-two scaled (common.cuh).
+// The ring stages hold this CTA's block of P2 mask words in the fragment-major tile layout; every
+// 16-row tile of a stage is one warp job: KT (= r/16) mma steps over 4 independent accumulators,
+// one 128-bit shared load of A and one 64-bit load of B per step.  The splits are summed per row
+// (hi + mid + lo), the logits go to zbuf, and after a consumer barrier one warp per mask word
+// ballots, writes the per-token words, the union word and its popcount.
 // ---------------------------------------------------------------------------
 struct P2Ctx {
   uint8_t *stages;
   uint64_t *full, *empty, *hready;
   float *zbuf, *s_b2;
   int *s_count;
-  float *sg;   // [B][r] shared staging of g
+  float *gs;        // [B][kt * 16] shared fp32 staging of g (zero-padded)
+  uint2 *gfrag;     // [kt][NT][32] shared B fragments
+  float *gscale;    // [B] shared
   unsigned long long *trace;
-  int NS, SB, st_p1, st_p2, w0, w1, m, r, words, words_p2, zst;
+  int NS, SB, st_p1, st_p2, w0, w1, m, r, kt, words, words_p2, zst;
   uint32_t ring0;
   float t;
   const float *g;
   uint32_t *mask, *uni;
 };
 
-template <typename T, int B, int CG>
+template <typename T, int B>
 __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
-  constexpr int RR = (B == 1) ? 4 : 2;   // rows per warp per iteration
-  constexpr int NV = Pow2Ceil<RR * B>::v;
+  constexpr int NT = (3 * B + 7) / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rchunks = x.r >> 3;
-  // g is read by every warp of every CTA: fetch it once per CTA (a 148-way instead of a
-  // 2368-way hot spot on the same L2 lines), then broadcast through shared memory
-  for (int i = tid * 4; i < B * x.r; i += kConsumers * 4)
-    *reinterpret_cast<float4 *>(x.sg + i) = __ldcg(reinterpret_cast<const float4 *>(x.g + i));
+  const int kt = x.kt, ldg = kt * 16;
+  // (1) g -> shared (once per CTA: a 148-way, not a 2368-way, hot spot on the same L2 lines)
+  for (int i = tid; i < B * ldg; i += kConsumers) {
+    const int b = i / ldg, k = i - b * ldg;
+    x.gs[i] = (k < x.r) ? __ldcg(x.g + (size_t)b * x.r + k) : 0.f;
+  }
   consumers_sync();
-  float gr[CG][8][B];
+  if (warp < B) {
+    float mx = 0.f;
+    for (int k = lane; k < x.r; k += 32) mx = fmaxf(mx, fabsf(x.gs[warp * ldg + k]));
 #pragma unroll
-  for (int q = 0; q < CG; ++q) {
-    const int ch = lane + q * 32;
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) x.gscale[warp] = g_scale<T>(mx);
+  }
+  consumers_sync();
+  // (2) B fragments
+  for (int e = tid; e < kt * NT * 32; e += kConsumers) {
+    const int K = e / (NT * 32), nt = (e / 32) % NT;
+    x.gfrag[e] = g_fragment<T, B>(x.gs, ldg, x.gscale, K, nt, e & 31);
+  }
+  consumers_sync();
+  float inv[B];
 #pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (ch < rchunks) {
-        const float4 a0 = *reinterpret_cast<const float4 *>(x.sg + (size_t)b * x.r + ch * 8);
-        const float4 a1 = *(reinterpret_cast<const float4 *>(x.sg + (size_t)b * x.r + ch * 8) + 1);
-        gr[q][0][b] = a0.x; gr[q][1][b] = a0.y; gr[q][2][b] = a0.z; gr[q][3][b] = a0.w;
-        gr[q][4][b] = a1.x; gr[q][5][b] = a1.y; gr[q][6][b] = a1.z; gr[q][7][b] = a1.w;
-      } else {
+  for (int b = 0; b < B; ++b) inv[b] = 1.f / x.gscale[b];
+  // (3) one warp per 16-row tile
+  const int rt_stage = 2 * x.words_p2;   // row tiles of a full stage
+  for (int job = warp; job < x.st_p2 * rt_stage; job += kConsumerWarps) {
+    const int st = job / rt_stage, j = job - st * rt_stage;
+    const int wa = x.w0 + st * x.words_p2, nw = min(x.w1, wa + x.words_p2) - wa;
+    if (j >= 2 * nw) continue;
+    const uint32_t it = x.st_p1 + st;
+    mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
+    if (x.trace && j == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
+    const uint8_t *a_base = x.stages + (size_t)(it % x.NS) * x.SB + (size_t)j * kt * kP2Tile + lane * 16;
+    const uint2 *b_base = x.gfrag + lane;
+    float acc[4][NT][4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) gr[q][e][b] = 0.f;
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[q][nt][v] = 0.f;
+    int K = 0;
+    for (; K + 4 <= kt; K += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 a = *reinterpret_cast<const uint4 *>(a_base + (size_t)(K + q) * kP2Tile);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) mma16816<T>(acc[q][nt], a, b_base[((K + q) * NT + nt) * 32]);
       }
     }
-  }
-  // the two warp groups (warps 0-7, 8-15) take alternate stages, so two stages are in flight
-  const int grp = warp >> 3, gw8 = warp & 7;
-  for (int st = grp; st < x.st_p2; st += 2) {
-    const uint32_t it = x.st_p1 + st;
-    const int wa = x.w0 + st * x.words_p2, wb = min(x.w1, wa + x.words_p2);
-    const int nrows = min(x.m, wb * 32) - wa * 32;
-    const int zoff = (wa - x.w0) * 32;   // CTA-local row of this stage's first row
-    mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
-    if (x.trace && tid == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
-    const uint8_t *buf = x.stages + (size_t)(it % x.NS) * x.SB;
-    for (int rb0 = gw8 * RR; rb0 < nrows; rb0 += kGroupWarps * RR) {
-      float v[NV];
+    for (; K < kt; ++K) {
+      const uint4 a = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
 #pragma unroll
-      for (int i = 0; i < NV; ++i) v[i] = 0.f;
-      Pack8 wv[RR][CG];
-#pragma unroll
-      for (int i = 0; i < RR; ++i)
-#pragma unroll
-        for (int q = 0; q < CG; ++q) {
-          const int ch = lane + q * 32;
-          wv[i][q] = lds128z(buf, (size_t)(rb0 + i) * x.r * 2 + (size_t)ch * 16, rb0 + i < nrows && ch < rchunks);
-        }
-#pragma unroll
-      for (int i = 0; i < RR; ++i)
-#pragma unroll
-        for (int q = 0; q < CG; ++q) {
-          float wf[8];
-          WT<T>::unpack(wv[i][q], wf);
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) v[b * RR + i] = fmaf(wf[e], gr[q][e][b], v[b * RR + i]);
-        }
-      const float z = warp_reduce_multi<NV>(v);   // lane l: token (l / RR) % B, row l % RR
-      if (lane < RR * B) x.zbuf[(lane / RR) * x.zst + zoff + rb0 + (lane % RR)] = z;
+      for (int nt = 0; nt < NT; ++nt) mma16816<T>(acc[0][nt], a, b_base[(K * NT + nt) * 32]);
     }
-    if (gw8 == 0 && lane == 0) mbar_arrive(&x.hready[it % x.NS]);   // keep hready phases = ring uses
+    float c[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) c[nt][v] = ((acc[0][nt][v] + acc[1][nt][v]) + acc[2][nt][v]) + acc[3][nt][v];
+    const int zrow = (wa - x.w0) * 32 + j * 16 + (lane >> 2);   // CTA-local row of (g)
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float z0, z1;
+      tile_logits<B, NT>(c, b, z0, z1);
+      if ((lane & 3) == 0) {
+        x.zbuf[b * x.zst + zrow] = z0 * inv[b];
+        x.zbuf[b * x.zst + zrow + 8] = z1 * inv[b];
+      }
+    }
     __syncwarp();
-    if (lane == 0) mbar_arrive_cnt(&x.empty[it % x.NS], 2);   // 8 warps of this group x 2
+    if (lane == 0) {
+      // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping)
+      if (j == 0) {
+        mbar_arrive(&x.hready[it % x.NS]);
+        mbar_arrive_cnt(&x.empty[it % x.NS], kConsumerWarps - 2 * nw + 1);
+      } else {
+        mbar_arrive(&x.empty[it % x.NS]);
+      }
+    }
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
   // ballots: one warp per mask word -> per-token words, union word, popcount
@@ -312,7 +335,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
   float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // [8][pcap*B] phase-4 partials
-  float *sg = s_part + 8 * p.pcap * B;                               // [B][r] staging of g
+  float *sg = s_part + 8 * p.pcap * B;                               // [B][kt*16] staging of g
+  uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
+  __shared__ float s_gscale[B];
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
@@ -358,7 +383,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
     };
-    const size_t rowb2 = (size_t)r * 2;
+    const size_t rowb2 = (size_t)p.kt * 16 * 2;   // bytes of one (padded) P2 row in the tiled layout
     for (int l = 0; l < L; ++l) {
       const LayerW lw = layer(l);
       if (l == (L > 1 ? 1 : 0)) trace_it0 = it;
@@ -377,7 +402,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         }
         const int s2 = max(0, NS - st_p1);
         if (s2 < st_p2) {
-          const size_t a0 = (size_t)(w0 + s2 * p.words_p2) * 32 * rowb2, a1 = (size_t)min(m, w1 * 32) * rowb2;
+          const size_t a0 = (size_t)(w0 + s2 * p.words_p2) * 32 * rowb2, a1 = (size_t)w1 * 32 * rowb2;
           for (size_t o = a0; o < a1; o += 32768)
             prefetch_l2(lw.p_w2 + o, (uint32_t)min((size_t)32768, a1 - o), keep);
         }
@@ -406,7 +431,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 rows of words [w0, w1), contiguous
         prefetch_tail(st_p1 + st);
         const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
-        const int ra = wa * 32, rb = min(m, wb * 32);
+        const int ra = wa * 32, rb = wb * 32;   // whole (zero-padded) words
         const uint32_t bytes = (uint32_t)((rb - ra) * rowb2);
         uint8_t *dst = acquire(bytes);
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
@@ -555,13 +580,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
-      P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, sg, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
-                r, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
-      const int cg = ((r >> 3) + 31) / 32;
-      if (cg <= 1) p2_phase<T, B, 1>(ctx);
-      else if (cg == 2) p2_phase<T, B, 2>(ctx);
-      else if (cg == 3) p2_phase<T, B, 3>(ctx);
-      else p2_phase<T, B, 4>(ctx);
+      P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, sg, gfrag, s_gscale, tr, NS, SB, (int)ring + st_p1,
+                st_p2, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
+      p2_phase<T, B>(ctx);
     }
     consumers_sync();
     if (tid == 0) {

@@ -46,13 +46,12 @@ constexpr int kConsumers = kConsumerWarps * 32;       // 512
 constexpr int kFusedThreads = kConsumers + 32;        // + producer warp
 constexpr int kFusedMaxB = 2;
 constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 16384)
-constexpr int kMaxCG = 4;        // 16-byte chunks of r per lane in phase 2 (r <= 1024)
 constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
 constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
 
 struct FusedWork {
   bool enabled = false;
-  int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0, part_off = 0, pcap = 0;
+  int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0, part_off = 0, pcap = 0, kt = 0;
   int d = 0, m = 0, r = 0;
   bool reglu = false;
   unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
@@ -101,6 +100,7 @@ struct FusedParams {
   int *counts;
   unsigned long long *bar;
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
+  int kt;                     // 16-column K tiles of the fragment-major P2 (ceil(r / 16))
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int hot_cap;                // at most this many hot neurons are L2-prefetched per layer
 };
@@ -120,29 +120,39 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.r = r;
   w.reglu = reglu;
   const int ch = fused_ch(d);
-  if (ch > kMaxCH || ch == 5 || ch == 7 || r > 8 * 32 * kMaxCG || d < 8 || r > 16 * num_sms || num_sms > 256)
+  if (ch > kMaxCH || ch == 5 || ch == 7 || d < 8 || r > 16 * num_sms || num_sms > 256)
     return true;  // unsupported shape: stays disabled (per-step kernels)
   w.P = num_sms;
-  // stage: >= one neuron (gate|up + down), one P2 word block, >= 32 KB
+  w.kt = (r + 15) / 16;
+  const size_t p2_word = (size_t)32 * w.kt * 16 * 2;   // one 32-row word of the tiled P2
+  // stage: >= one neuron (gate|up + down), one P2 word, >= 32 KB
   const size_t nb = (size_t)d * (reglu ? 6 : 4);
-  size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, (size_t)32 * r * 2});
+  size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, p2_word});
   sb = (sb + 127) / 128 * 128;
-  const size_t budget = 200 * 1024;
-  w.NS = (int)(budget / sb);
-  if (w.NS < 2) return true;
-  w.stage_bytes = (int)sb;
   // compaction stages the union words, the per-token words and the P counts in one ring slot
   if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)num_sms * 4 > sb) return true;
-  w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / ((size_t)32 * r * 2)));
+  w.stage_bytes = (int)sb;
+  w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / p2_word));
   w.idcap = (m + w.P - 1) / w.P + 2;
   const int words_all = (m + 31) / 32;
   w.wcap = (words_all + w.P - 1) / w.P + 1;
-  const size_t extra = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                       (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 +
-                       (size_t)w.idcap * 9;
-  w.part_off = (int)(((size_t)w.NS * sb + extra + 15) / 16 * 16);
   w.pcap = (d + w.P - 1) / w.P + 1;
-  w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * r * 4 + 64;
+  constexpr int NT = (3 * kFusedMaxB + 7) / 8;
+  // everything but the ring: mbarriers, reduction buffers, h, logits, b2, b_up/ids/bits, phase-4
+  // partials, g staging and its B fragments; the ring gets the rest (<= 200 KB)
+  auto extras = [&](int ns) {
+    return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * kFusedMaxB * 4 +
+           (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
+           (size_t)kFusedMaxB * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
+  };
+  const size_t cap = 227 * 1024 - 1024;   // static shared memory and alignment slack
+  w.NS = (int)std::min<size_t>(200 * 1024 / sb, cap / sb);
+  while (w.NS >= 2 && (size_t)w.NS * sb + extras(w.NS) > cap) --w.NS;
+  if (w.NS < 2) return true;
+  const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
+                     (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
+  w.part_off = (int)(((size_t)w.NS * sb + pre + 15) / 16 * 16);
+  w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, (size_t)(1 + num_sms) * 128 + 128)) return false;
   if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
@@ -232,6 +242,7 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.wcap = w.wcap;
   p.part_off = w.part_off;
   p.pcap = w.pcap;
+  p.kt = w.kt;
   p.trace = w.trace;
   p.hot_cap = a.hot_cap;
   return p;

@@ -70,68 +70,97 @@ __global__ void __launch_bounds__(256) k_predict1(const T *__restrict__ p1, cons
 }
 
 // ---------------------------------------------------------------------------
-// a2: z = P2 g + b2; bit = z > t; one warp per 32 neurons = one mask word.
-// Lane groups of LPR lanes share a row (LPR = power of two <= min(32, r/8)).
-// 128 threads = 4 words per block; g staged in shared memory.
+// a2: z = P2 g + b2; bit = z > t, on the tensor cores (mma.m16n8k16 over the fragment-major P2,
+// g split into three 16-bit parts; common.cuh).  256 threads = 8 warps = 8 row tiles of 16 =
+// 4 mask words per block; g's B fragments are built once per block in shared memory; each
+// warp streams its tile row of P2 straight from HBM (one 128-bit load per lane and K tile).
 // ---------------------------------------------------------------------------
 template <typename T, int B>
-__global__ void __launch_bounds__(128) k_predict2(const T *__restrict__ p2, const T *__restrict__ b2,
-                                                   const float *__restrict__ g, float t, int m,
-                                                   int r, int words, uint32_t *__restrict__ mask,
+__global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, const T *__restrict__ b2,
+                                                   const float *__restrict__ g, float t, int m, int r, int kt,
+                                                   int words, uint32_t *__restrict__ mask,
                                                    float *__restrict__ logits) {
-  extern __shared__ float p2smem[];
-  float *gs = p2smem;                     // [B][r]
-  float *zb = p2smem + B * r;             // [4 warps][B][32]
-  for (int i = threadIdx.x; i < B * r; i += blockDim.x) gs[i] = g[i];
-  __syncthreads();
+  constexpr int NT = (3 * B + 7) / 8;
+  extern __shared__ __align__(16) float p2smem[];
+  const int ldg = kt * 16;
+  float *gs = p2smem;                                          // [B][ldg]
+  uint2 *gfrag = reinterpret_cast<uint2 *>(gs + B * ldg);       // [kt][NT][32]
+  float *zb = reinterpret_cast<float *>(gfrag + kt * NT * 32);  // [B][128]
+  __shared__ float gscale[B];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int word = blockIdx.x * 4 + warp;
-  if (word >= words) return;
-  const int chunks = r >> 3;
-  int lpr = 1;
-  while (lpr * 2 <= chunks && lpr < 32) lpr *= 2;
-  const int rp = 32 / lpr;                // rows in flight per warp iteration
-  const int q = lane / lpr, sl = lane % lpr;
-  float *zw = zb + warp * B * 32;
-  for (int it = 0; it < 32 / rp; ++it) {
-    const int rin = it * rp + q;
-    const int i = word * 32 + rin;
-    float acc[B];
+  for (int i = threadIdx.x; i < B * ldg; i += blockDim.x) {
+    const int b = i / ldg, k = i - b * ldg;
+    gs[i] = (k < r) ? g[(int64_t)b * r + k] : 0.f;
+  }
+  __syncthreads();
+  if (warp < B) {
+    float mx = 0.f;
+    for (int k = lane; k < r; k += 32) mx = fmaxf(mx, fabsf(gs[warp * ldg + k]));
 #pragma unroll
-    for (int b = 0; b < B; ++b) acc[b] = 0.f;
-    if (i < m) {
-      const T *w = p2 + (int64_t)i * r;
-#pragma unroll 2
-      for (int c = sl; c < chunks; c += lpr) {
-        float wf[8];
-        WT<T>::unpack(ld_stream(w + c * 8), wf);
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) gscale[warp] = g_scale<T>(mx);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kt * NT * 32; e += blockDim.x)
+    gfrag[e] = g_fragment<T, B>(gs, ldg, gscale, e / (NT * 32), (e / 32) % NT, e & 31);
+  __syncthreads();
+  const int R = blockIdx.x * 8 + warp;   // global row tile
+  if (R * 16 < words * 32) {
+    const uint8_t *a_base = reinterpret_cast<const uint8_t *>(p2t) + (size_t)R * kt * kP2Tile + lane * 16;
+    float acc[4][NT][4];
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-          const float *gb = gs + b * r + c * 8;
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) acc[b] = fmaf(wf[k], gb[k], acc[b]);
-        }
-      }
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[q][nt][v] = 0.f;
+    int K = 0;
+    for (; K + 4 <= kt; K += 4) {
+      Pack8 a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = ld_stream(a_base + (size_t)(K + q) * kP2Tile);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          mma16816<T>(acc[q][nt], make_uint4(a[q].u[0], a[q].u[1], a[q].u[2], a[q].u[3]),
+                      gfrag[((K + q) * NT + nt) * 32 + lane]);
     }
+    for (; K < kt; ++K) {
+      const Pack8 a = ld_stream(a_base + (size_t)K * kP2Tile);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        mma16816<T>(acc[0][nt], make_uint4(a.u[0], a.u[1], a.u[2], a.u[3]), gfrag[(K * NT + nt) * 32 + lane]);
+    }
+    float c[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) c[nt][v] = ((acc[0][nt][v] + acc[1][nt][v]) + acc[2][nt][v]) + acc[3][nt][v];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      float v = acc[b];
-      for (int o = lpr >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (sl == 0) {
-        float z = __int_as_float(0x7fc00000);          // NaN: never active
-        if (i < m) z = v + (b2 ? WT<T>::to_float(b2, i) : 0.f);
-        zw[b * 32 + rin] = z;
+      float z0, z1;
+      tile_logits<B, NT>(c, b, z0, z1);
+      if ((lane & 3) == 0) {
+        const float inv = 1.f / gscale[b];
+        zb[b * 128 + warp * 16 + (lane >> 2)] = z0 * inv;
+        zb[b * 128 + warp * 16 + (lane >> 2) + 8] = z1 * inv;
       }
     }
   }
-  __syncwarp();
-  const int i = word * 32 + lane;
+  __syncthreads();
+  if (warp < 4) {
+    const int word = blockIdx.x * 4 + warp;
+    if (word >= words) return;
+    const int i = word * 32 + lane;
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
-    const float z = zw[b * 32 + lane];
-    const uint32_t bits = __ballot_sync(0xffffffffu, z > t);
-    if (lane == 0) mask[(int64_t)b * words + word] = bits;
-    if (logits && i < m) logits[(int64_t)b * m + i] = z;
+    for (int b = 0; b < B; ++b) {
+      float z = __int_as_float(0x7fc00000);          // NaN: never active
+      if (i < m) z = zb[b * 128 + warp * 32 + lane] + (b2 ? WT<T>::to_float(b2, i) : 0.f);
+      const uint32_t bits = __ballot_sync(0xffffffffu, z > t);
+      if (lane == 0) mask[(int64_t)b * words + word] = bits;
+      if (logits && i < m) logits[(int64_t)b * m + i] = z;
+    }
   }
 }
 
@@ -304,10 +333,14 @@ cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float 
       k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const size_t smem = (size_t)(NB * a.r + 4 * NB * 32) * 4;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_predict2<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_predict2<T, NB><<<(a.words + 3) / 4, 128, smem, s>>>((const T *)a.p_w2, (const T *)a.p_b2, a.g, a.t, a.m,
-                                                           a.r, a.words, mask, logits);
+    constexpr int NT = (3 * NB + 7) / 8;
+    const size_t smem = (size_t)NB * a.kt * 16 * 4 + (size_t)a.kt * NT * 32 * 8 + (size_t)NB * 128 * 4;
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(k_predict2<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_predict2<T, NB><<<(a.words + 3) / 4, 256, smem, s>>>((const T *)a.p_w2, (const T *)a.p_b2, a.g, a.t, a.m,
+                                                           a.r, a.kt, a.words, mask, logits);
     return cudaGetLastError();
   });
 }

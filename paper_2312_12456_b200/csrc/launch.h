@@ -14,7 +14,7 @@ struct StepArgs {
   const void *p_w1, *p_b1, *p_w2, *p_b2, *w_up, *b_up, *w_down, *b_down;
   float *g, *h, *partial;
   unsigned *tickets;
-  int d, m, r, words, S, tiles, num_sms;
+  int d, m, r, kt, words, S, tiles, num_sms;
   float t;
   bool pred_relu, reglu;
 };
@@ -32,6 +32,7 @@ cudaError_t launch_rms_scale(const float *x, int B, int d, float *scale, cudaStr
 cudaError_t launch_compact(const uint32_t *mask, int B, int words, int32_t *ids, int32_t *n_active, cudaStream_t s);
 cudaError_t launch_gather_rows(const void *src, const int32_t *nid, int rows, int cols, int64_t dst_stride,
                                int dst_off, void *dst, cudaStream_t s);
+cudaError_t launch_tile_p2(const void *src, const int32_t *nid, int rows, int cols, void *dst, cudaStream_t s);
 cudaError_t launch_transpose_gather(const void *src, const int32_t *nid, int d, int m_total, int m_local,
                                     void *dst, cudaStream_t s);
 

@@ -1,5 +1,7 @@
 // misc.cu -- libpi's non-templated kernels: the RMS input scale, the single-CTA compaction used
 // by pi_compact and the per-step path, and the create-time repacking kernels.
+#include <algorithm>
+
 #include "launch.h"
 
 namespace pi {
@@ -110,6 +112,32 @@ __global__ void k_transpose_gather(const uint16_t *__restrict__ src, const int32
     const int k = k0 + kk, j = j0 + threadIdx.x;
     if (k < m_local && j < d) dst[(int64_t)k * d + j] = tileb[threadIdx.x][kk];
   }
+}
+
+// Fragment-major P2 (common.cuh): dst[p2_tiled_index(k, j, kt)] = src[nid[k], j] for k < rows,
+// j < cols; rows padded to a multiple of 32 and columns to kt * 16 with zeros.
+__global__ void k_tile_p2(const uint16_t *__restrict__ src, const int32_t *__restrict__ nid, int rows, int cols,
+                          int rows_pad, int kt, uint16_t *__restrict__ dst) {
+  const int64_t n = (int64_t)rows_pad * kt * 16;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t blk = o >> 8;
+    const int within = (int)(o & 255), lane = within >> 3, e = within & 7;
+    const int R = (int)(blk / kt), K = (int)(blk % kt);
+    const int g = lane >> 2, t = lane & 3;
+    const int row = 16 * R + g + ((e >> 1) & 1) * 8;
+    const int col = 16 * K + 2 * t + (e & 1) + (e >> 2) * 8;
+    uint16_t v = 0;
+    if (row < rows && col < cols) v = src[(int64_t)(nid ? nid[row] : row) * cols + col];
+    dst[o] = v;
+  }
+}
+
+cudaError_t launch_tile_p2(const void *src, const int32_t *nid, int rows, int cols, void *dst, cudaStream_t s) {
+  const int rows_pad = (rows + 31) / 32 * 32, kt = (cols + 15) / 16;
+  const int64_t n = (int64_t)rows_pad * kt * 16;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_tile_p2<<<grid, 256, 0, s>>>((const uint16_t *)src, nid, rows, cols, rows_pad, kt, (uint16_t *)dst);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rms_scale(const float *x, int B, int d, float *scale, cudaStream_t s) {

@@ -225,7 +225,9 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   if (D->b_down) ALLOC(L->b_down, (size_t)d * e, true);
   ALLOC(L->p_w1, (size_t)r * d * e, true);
   if (D->p_b1) ALLOC(L->p_b1, (size_t)r * e, true);
-  ALLOC(L->p_w2, (size_t)ml * r * e, true);
+  // P2 in the fragment-major tile layout of the tensor-core GEMV (common.cuh): rows padded to whole
+  // mask words, columns to 16
+  ALLOC(L->p_w2, (size_t)L->words * 32 * ((r + 15) / 16 * 16) * e, true);
   if (D->p_b2) ALLOC(L->p_b2, (size_t)ml * e, true);
 
   // down-projection split: ~4 blocks per SM in total
@@ -289,7 +291,10 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   } else {
     gather(D->w_up, L->w_up, d, d, 0);
   }
-  gather(D->p_w2, L->p_w2, r, r, 0);
+  {
+    const cudaError_t e2 = launch_tile_p2(D->p_w2, d_nid, ml, r, L->p_w2, s);
+    if (ge == cudaSuccess) ge = e2;
+  }
   if (D->b_up) gather(D->b_up, L->b_up, 1, 1, 0);
   if (D->p_b2) gather(D->p_b2, L->p_b2, 1, 1, 0);
   {
@@ -487,7 +492,7 @@ static StepArgs step_args(const pi_layer *L) {
   a.p_w1 = L->p_w1; a.p_b1 = L->p_b1; a.p_w2 = L->p_w2; a.p_b2 = L->p_b2;
   a.w_up = L->w_up; a.b_up = L->b_up; a.w_down = L->w_down; a.b_down = L->b_down;
   a.g = L->g; a.h = L->h; a.partial = L->partial; a.tickets = L->tickets;
-  a.d = L->d; a.m = L->m_local; a.r = L->r; a.words = L->words; a.S = L->S; a.tiles = L->tiles;
+  a.d = L->d; a.m = L->m_local; a.r = L->r; a.kt = (L->r + 15) / 16; a.words = L->words; a.S = L->S; a.tiles = L->tiles;
   a.num_sms = L->num_sms; a.t = L->threshold;
   a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
   return a;

@@ -64,7 +64,9 @@ def _worker(rank, world, port, q, kind, args):
         st.step(x, y, n_out, record=rec)
         torch.cuda.synchronize()
         # (gloo collectives are not CUDA-graph capturable; Stack.capture is covered with NCCL / world 1)
-        q.put((rank, {"y": y.cpu(), "rec": [t.cpu() for t in rec], "n": n_out.cpu()}))
+        # numpy (pickled by value): torch CPU tensors would travel as shared-memory handles that die
+        # with this process
+        q.put((rank, {"y": y.cpu().numpy(), "rec": [t.cpu().numpy() for t in rec], "n": n_out.cpu().numpy()}))
         st.close()
         dist.barrier()
         dist.destroy_process_group()
@@ -103,7 +105,7 @@ def test_sharded_step_integer_layer_bitwise(world, act):
     om, _ = O.predict(x, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), 0.5)
     yo = O.sparse_ffn(x, O.compact(om), om, f(w.w_up), f(w.b_up), f(w.w_gate), f(w.w_down), f(w.b_down), act)
     for rk in range(world):
-        assert (res[rk]["y"].numpy() == yo).all(), rk
+        assert (res[rk]["y"] == yo).all(), rk
     assert sum(int(res[rk]["n"][0]) for rk in range(world)) == len(O.compact(om))
 
 
@@ -113,9 +115,9 @@ def test_sharded_step_random_stack(world):
     from paper_2312_12456_b200.stack import build_stack
     name, dims, n_layers, B = "c4", {"d": 1024, "m": 4096, "r": 64}, 3, 2
     res = _run(world, "rand", (name, dims, n_layers, B))
-    y0 = res[0]["y"].numpy()
+    y0 = res[0]["y"]
     for rk in range(1, world):
-        assert (res[rk]["y"].numpy() == y0).all(), "ranks disagree after the all-reduce"
+        assert (res[rk]["y"] == y0).all(), "ranks disagree after the all-reduce"
     # unsharded GPU stack (world 1, one persistent launch) on the same weights and token
     cfg = gen.CONFIGS[name]
     st, kept = build_stack(cfg, n_layers=n_layers, seed=4, device="cuda", max_batch=B, keep_weights=True, dims=dims)
@@ -125,7 +127,7 @@ def test_sharded_step_random_stack(world):
     st.step(x, y, n1)
     torch.cuda.synchronize()
     assert O.rel_l2(y0, y.cpu().numpy()) <= GATE
-    n_sh = sum(res[rk]["n"].numpy() for rk in range(world))
+    n_sh = sum(res[rk]["n"] for rk in range(world))
     assert (np.abs(n_sh - n1.cpu().numpy()) <= 2).all(), (n_sh, n1)   # equal up to near-threshold flips
     # each layer's merged output against the unsharded oracle on that layer's GPU input (R20)
     cur = f(x).astype(np.float64)
@@ -133,7 +135,7 @@ def test_sharded_step_random_stack(world):
         xo = O.rms_normalize(cur) if cfg.rmsnorm else cur
         om, z = O.predict(xo, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), w.threshold)
         yo = O.sparse_ffn(xo, O.compact(om), om, f(w.w_up), f(w.b_up), f(w.w_gate), f(w.w_down), f(w.b_down), w.act)
-        yl = res[0]["rec"][l].numpy()
+        yl = res[0]["rec"][l]
         if not O.near_threshold(z, w.threshold).any():
             err = O.rel_l2(yl, yo)
             assert err <= TOL and err <= GATE, (l, err)
