@@ -201,12 +201,15 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   constexpr int NT = (3 * B + 7) / 8;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kt = x.kt, ldg = kt * 16;
+  unsigned long long *dt = (x.trace && lane == 0) ? x.trace + 128 : nullptr;   // phase-2 detail (tracing)
+  if (dt && warp == 0) dt[0] = globaltimer();
   // (1) g -> shared (once per CTA: a 148-way, not a 2368-way, hot spot on the same L2 lines)
   for (int i = tid; i < B * ldg; i += kConsumers) {
     const int b = i / ldg, k = i - b * ldg;
     x.gs[i] = (k < x.r) ? __ldcg(x.g + (size_t)b * x.r + k) : 0.f;
   }
   consumers_sync();
+  if (dt && warp == 0) dt[1] = globaltimer();
   if (warp < B) {
     float mx = 0.f;
     for (int k = lane; k < x.r; k += 32) mx = fmaxf(mx, fabsf(x.gs[warp * ldg + k]));
@@ -221,18 +224,30 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     x.gfrag[e] = g_fragment<T, B>(x.gs, ldg, x.gscale, K, nt, e & 31);
   }
   consumers_sync();
+  if (dt && warp == 0) dt[2] = globaltimer();
+  bool first_job = true;
   float inv[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) inv[b] = 1.f / x.gscale[b];
-  // (3) one warp per 16-row tile
+  // (3) one warp per 16-row tile.  Jobs go round-robin over the warps in rounds of at most NS
+  // stages, with a consumer barrier between rounds: a warp may only wait on a ring position whose
+  // previous use (NS positions back) is known to be filled, or the mbarrier parity would alias.
   const int rt_stage = 2 * x.words_p2;   // row tiles of a full stage
-  for (int job = warp; job < x.st_p2 * rt_stage; job += kConsumerWarps) {
-    const int st = job / rt_stage, j = job - st * rt_stage;
+  for (int s0 = 0; s0 < x.st_p2; s0 += x.NS) {
+  const int s1 = min(x.st_p2, s0 + x.NS);
+  if (s0 > 0) consumers_sync();
+  for (int job = warp; job < (s1 - s0) * rt_stage; job += kConsumerWarps) {
+    const int st = s0 + job / rt_stage, j = job % rt_stage;
     const int wa = x.w0 + st * x.words_p2, nw = min(x.w1, wa + x.words_p2) - wa;
     if (j >= 2 * nw) continue;
     const uint32_t it = x.st_p1 + st;
     mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
     if (x.trace && j == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
+    long long c_job = 0;
+    if (dt && first_job) {
+      dt[16 + warp] = globaltimer();
+      c_job = clock64();
+    }
     const uint8_t *a_base = x.stages + (size_t)(it % x.NS) * x.SB + (size_t)j * kt * kP2Tile + lane * 16;
     const uint2 *b_base = x.gfrag + lane;
     float acc[4][NT][4];
@@ -261,6 +276,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int v = 0; v < 4; ++v) c[nt][v] = ((acc[0][nt][v] + acc[1][nt][v]) + acc[2][nt][v]) + acc[3][nt][v];
+    if (dt && first_job) dt[32 + warp] = (unsigned long long)(clock64() - c_job) + (c[0][0] == 1.2345e-30f ? 1 : 0);
     const int zrow = (wa - x.w0) * 32 + j * 16 + (lane >> 2);   // CTA-local row of (g)
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -281,8 +297,12 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
         mbar_arrive(&x.empty[it % x.NS]);
       }
     }
+    if (dt && first_job) dt[48 + warp] = globaltimer();
+    first_job = false;
+  }
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
+  if (dt && warp == 0) dt[3] = globaltimer();
   // ballots: one warp per mask word -> per-token words, union word, popcount
   int my_count = 0;
   for (int wl = warp; wl < x.w1 - x.w0; wl += kConsumerWarps) {

@@ -62,6 +62,7 @@ def main():
         issue = np.where(full[:, 72:128] > 0, (full[:, 72:128] - t0) / 1e3, np.nan)
         stage_rows.append((ready, issue))
         gl = full[:, 200]
+        p2d = full[:, 128:192].copy()
         bars = [full[:, 204 + 4 * k:208 + 4 * k].copy() for k in range(4)]
         raw = full[:, 128:192].reshape(P, 16, 4)
         base = raw[:, 0, 3:4]
@@ -81,6 +82,19 @@ def main():
         rel_done = (bk[:, 3] - t0) / 1e3
         out[nm + "_cycles_atomret_flagseen_median"] = [float(np.median(bk[:, 1])), float(np.median(bk[:, 2]))]
         out[nm + "_release_us_min_max"] = [float(rel_done.min()), float(rel_done.max())]
+    # phase-2 detail (fused.cuh p2_phase, last rep): us relative to the phase-2 entry, median over CTAs
+    d0 = p2d[:, 0:1]
+    rel = lambda a: np.where(a > 0, (a - d0) / 1e3, np.nan)  # noqa: E731
+    out["p2_detail_us_median_over_ctas"] = {
+        "g staged": float(np.nanmedian(rel(p2d[:, 1:2]))), "B fragments built": float(np.nanmedian(rel(p2d[:, 2:3]))),
+        "first job start (min/max warp)": [float(np.nanmedian(np.nanmin(rel(p2d[:, 16:32]), axis=1))),
+                                          float(np.nanmedian(np.nanmax(rel(p2d[:, 16:32]), axis=1)))],
+        "first job end (min/max warp)": [float(np.nanmedian(np.nanmin(rel(p2d[:, 48:64]), axis=1))),
+                                        float(np.nanmedian(np.nanmax(rel(p2d[:, 48:64]), axis=1)))],
+        "mma loop cycles (median/max warp)": [float(np.nanmedian(np.where(p2d[:, 32:48] > 0, p2d[:, 32:48], np.nan))),
+                                             float(np.nanmedian(np.nanmax(np.where(p2d[:, 32:48] > 0, p2d[:, 32:48], np.nan), axis=1)))],
+        "all logits in zbuf": float(np.nanmedian(rel(p2d[:, 3:4]))),
+        "P2 done (ballots)": float(np.nanmedian((full[:, 3] - p2d[:, 0]) / 1e3))}
     rd, iss = stage_rows[-1]
     for cta in (0, P // 2):
         k = int(np.sum(~np.isnan(rd[cta])))
