@@ -310,3 +310,45 @@ def int_tokens(B: int, d: int, act: str = "relu", seed: int = 0, device="cpu") -
     g = torch.Generator().manual_seed(seed + 12345)
     a = 3 if act == "relu" else 2
     return torch.randint(-a, a + 1, (B, d), generator=g).to(torch.float32).to(device)
+
+
+# ---------------------------------------------------------------------------
+# INT4 neuron rows (row f3; format: DESIGN.md reading R21, oracle/quant.py): model preparation,
+# i.e. input generation -- the method's arithmetic (dequantise + FFN) runs in libpi / the oracle.
+# ---------------------------------------------------------------------------
+Q4_GROUP = 32
+
+
+def quantize_q4(w: torch.Tensor):
+    """Symmetric 4-bit quantisation of rows [rows, d] (d % 32 == 0) in groups of 32: scale =
+    fp16(max|w| / 7), code = clamp(round(w / scale), -8, 7) + 8, two codes per byte (element 2k in
+    the low nibble of byte k).  Returns (codes uint8 [rows, d/2], scales fp16 [rows, d/32])."""
+    rows, d = w.shape
+    assert d % Q4_GROUP == 0
+    wf = w.float().reshape(rows, d // Q4_GROUP, Q4_GROUP)
+    amax = wf.abs().amax(dim=2)
+    scale = (amax / 7.0).to(torch.float16)
+    s = scale.float()
+    q = torch.where(s[..., None] > 0, torch.round(wf / torch.where(s > 0, s, 1.0)[..., None]), torch.zeros_like(wf))
+    q = (q.clamp(-8, 7) + 8).to(torch.uint8).reshape(rows, d)
+    codes = (q[:, 0::2] | (q[:, 1::2] << 4)).contiguous()
+    return codes, scale.contiguous()
+
+
+@dataclasses.dataclass
+class Q4Weights:
+    """The FFN of one layer as INT4 neuron rows (neuron-major: row i = neuron i's d-vector)."""
+    up_codes: torch.Tensor
+    up_scales: torch.Tensor
+    gate_codes: Optional[torch.Tensor]
+    gate_scales: Optional[torch.Tensor]
+    down_codes: torch.Tensor            # neuron i's down column W_down[:, i] as a row
+    down_scales: torch.Tensor
+
+
+def make_q4(w: "LayerWeights") -> Q4Weights:
+    """Quantise a generated layer's FFN matrices (the predictor keeps its 16-bit weights)."""
+    uc, us = quantize_q4(w.w_up)
+    gc, gs = quantize_q4(w.w_gate) if w.w_gate is not None else (None, None)
+    dc, ds = quantize_q4(w.w_down.t().contiguous())
+    return Q4Weights(uc, us, gc, gs, dc, ds)
