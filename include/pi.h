@@ -54,6 +54,14 @@ typedef enum {
 } pi_status;
 
 typedef enum { PI_DT_F16 = 0, PI_DT_BF16 = 1 } pi_dtype;
+/* FFN weight format.  PI_FFN_16: w_up / w_gate / w_down hold `dtype` values in the nn.Linear
+ * layouts below.  PI_FFN_Q4: INT4 weight-only neuron rows ("FP16 and INT4 quantized
+ * parameters"; "Inference with Quantization"; format = DESIGN.md reading
+ * R21): every neuron's d-vector -- its up row, gate row and down COLUMN -- is given as a row of
+ * d/2 code bytes (neuron-major [m_total, d/2] uint8; element 2k in the low nibble of byte k)
+ * plus d/32 fp16 scales (*_scale, [m_total, d/32]); w = scale[j / 32] * (code_j - 8).  The
+ * predictor, b_up and b_down stay in `dtype`.  d % 32 == 0. */
+typedef enum { PI_FFN_16 = 0, PI_FFN_Q4 = 1 } pi_ffn_format;
 /* PI_ACT_RELU: h = relu(a).  PI_ACT_REGLU: h = relu(W_gate[i].x) * a (reading R5). */
 typedef enum { PI_ACT_RELU = 0, PI_ACT_REGLU = 1 } pi_act;
 /* predictor hidden non-linearity (P:555 names only "a single hidden" layer; reading R1) */
@@ -107,6 +115,10 @@ typedef struct {
   const float *neuron_freq;
   float hot_freq;
   int32_t hot_cap;
+  pi_ffn_format ffn_format;  /* PI_FFN_16 (default, 0) or PI_FFN_Q4                         */
+  const void *w_up_scale;    /* PI_FFN_Q4: dev fp16 [m_total, d/32]; else NULL               */
+  const void *w_gate_scale;  /* PI_FFN_Q4 and REGLU: dev fp16 [m_total, d/32]; else NULL     */
+  const void *w_down_scale;  /* PI_FFN_Q4: dev fp16 [m_total, d/32]; else NULL               */
 } pi_layer_desc;
 
 typedef struct {
@@ -117,6 +129,7 @@ typedef struct {
   int64_t weight_bytes;     /* library-owned weight bytes on the device             */
   int64_t workspace_bytes;  /* library-owned workspace bytes                        */
   int32_t launches_per_forward; /* kernel launches one pi_layer_forward call makes   */
+  int32_t ffn_format;           /* pi_ffn_format                                      */
 } pi_layer_info;
 
 /* Library version string, e.g. "libpi 0.1.0 sm_100a". */

@@ -183,11 +183,11 @@ __device__ __forceinline__ float up_total(const float *red, int i) {
 struct P2Ctx {
   uint8_t *stages;
   uint64_t *full, *empty, *hready;
+  volatile uint32_t *slot_pos;   // [NS] ring position the producer last acquired each slot for
   float *zbuf, *s_b2;
   int *s_count;
-  float *gs;        // [B][kt * 16] shared fp32 staging of g (zero-padded)
-  uint2 *gfrag;     // [kt][NT][32] shared B fragments
-  float *gscale;    // [B] shared
+  uint2 *gfrag;                  // [kt][NT][32] shared B fragments
+  unsigned *gmax;                // [B] shared max |g| bits (fp16 scaling), zeroed at layer start
   unsigned long long *trace;
   int NS, SB, st_p1, st_p2, w0, w1, m, r, kt, words, words_p2, zst;
   uint32_t ring0;
@@ -199,107 +199,141 @@ struct P2Ctx {
 template <typename T, int B>
 __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   constexpr int NT = (3 * B + 7) / 8;
+  static_assert(NT == 1, "fused phase 2 handles B <= 2 (one n tile)");
+  constexpr bool kScaled = std::is_same<T, __half>::value;   // fp16 needs the range scale (common.cuh)
+  constexpr int kUL = 12 * B;    // lanes of a K tile whose column n = lane / 4 < 3 B (the rest stay zero)
+  constexpr int kMaxE = 3;       // useful B fragment entries per consumer thread (fused_alloc: kt * 12 B <= 1536)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kt = x.kt, ldg = kt * 16;
+  const int kt = x.kt, ne = kt * kUL;
   unsigned long long *dt = (x.trace && lane == 0) ? x.trace + 128 : nullptr;   // phase-2 detail (tracing)
   if (dt && warp == 0) dt[0] = globaltimer();
-  // (1) g -> shared (once per CTA: a 148-way, not a 2368-way, hot spot on the same L2 lines)
-  for (int i = tid; i < B * ldg; i += kConsumers) {
-    const int b = i / ldg, k = i - b * ldg;
-    x.gs[i] = (k < x.r) ? __ldcg(x.g + (size_t)b * x.r + k) : 0.f;
-  }
-  consumers_sync();
-  if (dt && warp == 0) dt[1] = globaltimer();
-  if (warp < B) {
-    float mx = 0.f;
-    for (int k = lane; k < x.r; k += 32) mx = fmaxf(mx, fabsf(x.gs[warp * ldg + k]));
+  // (1) B fragments straight from g in global memory (one L2 round trip): useful entry u =
+  // (K tile, lane L < 12 B) needs g[b][16K + 2t + {0,1,8,9}] of token b = (L / 4) / 3
+  float gv[kMaxE][4];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) x.gscale[warp] = g_scale<T>(mx);
+  for (int q = 0; q < kMaxE; ++q) {
+    const int u = tid + q * kConsumers;
+    const int K = u / kUL, L = u % kUL, n = L >> 2, t = L & 3;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int kk = K * 16 + 2 * t + (v & 1) + (v >> 1) * 8;
+      gv[q][v] = (u < ne && kk < x.r) ? __ldcg(x.g + (size_t)(n / 3) * x.r + kk) : 0.f;
+    }
   }
-  consumers_sync();
-  // (2) B fragments
-  for (int e = tid; e < kt * NT * 32; e += kConsumers) {
-    const int K = e / (NT * 32), nt = (e / 32) % NT;
-    x.gfrag[e] = g_fragment<T, B>(x.gs, ldg, x.gscale, K, nt, e & 31);
+  float sc[B];
+#pragma unroll
+  for (int b = 0; b < B; ++b) sc[b] = 1.f;
+  if (kScaled) {
+    // per-token max |g| (split-0 entries cover every value once): shared atomicMax on the bits
+#pragma unroll
+    for (int q = 0; q < kMaxE; ++q) {
+      const int u = tid + q * kConsumers, n = (u % kUL) >> 2;
+      if (u < ne && n % 3 == 0) {
+        float mx = 0.f;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) mx = fmaxf(mx, fabsf(gv[q][v]));
+        atomicMax(x.gmax + n / 3, __float_as_uint(mx));
+      }
+    }
+    consumers_sync();
+#pragma unroll
+    for (int b = 0; b < B; ++b) sc[b] = g_scale<T>(__uint_as_float(x.gmax[b]));
+  }
+#pragma unroll
+  for (int q = 0; q < kMaxE; ++q) {
+    const int u = tid + q * kConsumers;
+    if (u < ne) {
+      const int K = u / kUL, L = u % kUL, n = L >> 2, b = n / 3, s = n % 3;
+      const float s_b = (B == 1 || b == 0) ? sc[0] : sc[B - 1];
+      uint32_t r2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint16_t p0[3], p1[3];
+        Split3<T>::split(gv[q][2 * h] * s_b, p0);
+        Split3<T>::split(gv[q][2 * h + 1] * s_b, p1);
+        r2[h] = (uint32_t)p0[s] | ((uint32_t)p1[s] << 16);
+      }
+      x.gfrag[K * 32 + L] = make_uint2(r2[0], r2[1]);
+    }
   }
   consumers_sync();
   if (dt && warp == 0) dt[2] = globaltimer();
   bool first_job = true;
   float inv[B];
 #pragma unroll
-  for (int b = 0; b < B; ++b) inv[b] = 1.f / x.gscale[b];
-  // (3) one warp per 16-row tile.  Jobs go round-robin over the warps in rounds of at most NS
-  // stages, with a consumer barrier between rounds: a warp may only wait on a ring position whose
-  // previous use (NS positions back) is known to be filled, or the mbarrier parity would alias.
-  const int rt_stage = 2 * x.words_p2;   // row tiles of a full stage
-  for (int s0 = 0; s0 < x.st_p2; s0 += x.NS) {
-  const int s1 = min(x.st_p2, s0 + x.NS);
-  if (s0 > 0) consumers_sync();
-  for (int job = warp; job < (s1 - s0) * rt_stage; job += kConsumerWarps) {
-    const int st = s0 + job / rt_stage, j = job % rt_stage;
-    const int wa = x.w0 + st * x.words_p2, nw = min(x.w1, wa + x.words_p2) - wa;
-    if (j >= 2 * nw) continue;
+  for (int b = 0; b < B; ++b) inv[b] = 1.f / sc[b];
+  // (2) one warp per mask word (two 16-row tiles sharing each B fragment), round-robin over the
+  // warps.  A warp may reach a ring position while its slot still holds an older stage: it first
+  // waits until the producer has acquired the slot for this position (slot_pos), after which the
+  // full barrier's parity is unambiguous.
+  const int wpp = x.words_p2;
+  for (int job = warp; job < x.st_p2 * wpp; job += kConsumerWarps) {
+    const int st = job / wpp, j = job - st * wpp;   // word j of stage st
+    const int wa = x.w0 + st * wpp, nw = min(x.w1, wa + wpp) - wa;
+    if (j >= nw) continue;
     const uint32_t it = x.st_p1 + st;
-    mbar_wait(&x.full[it % x.NS], (it / x.NS) & 1);
+    const int slot = it % x.NS;
+    while (x.slot_pos[slot] != it) __nanosleep(20);
+    mbar_wait(&x.full[slot], (it / x.NS) & 1);
     if (x.trace && j == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
     long long c_job = 0;
     if (dt && first_job) {
       dt[16 + warp] = globaltimer();
       c_job = clock64();
     }
-    const uint8_t *a_base = x.stages + (size_t)(it % x.NS) * x.SB + (size_t)j * kt * kP2Tile + lane * 16;
+    const uint8_t *a_base = x.stages + (size_t)slot * x.SB + (size_t)(2 * j) * kt * kP2Tile + lane * 16;
     const uint2 *b_base = x.gfrag + lane;
-    float acc[4][NT][4];
+    float acc[2][2][NT][4];   // [row tile][chain][n tile][reg]
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[rt][q][nt][v] = 0.f;
+#pragma unroll 2
+    for (int K = 0; K < kt; ++K) {
+      const uint4 a0 = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
+      const uint4 a1 = *reinterpret_cast<const uint4 *>(a_base + (size_t)(kt + K) * kP2Tile);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const uint2 b = b_base[(K * NT + nt) * 32];
+        mma16816<T>(acc[0][K & 1][nt], a0, b);
+        mma16816<T>(acc[1][K & 1][nt], a1, b);
+      }
+    }
+    if (dt && first_job) dt[32 + warp] = (unsigned long long)(clock64() - c_job) + (acc[0][0][0][0] == 1.2345e-30f ? 1 : 0);
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt) {
+      float c[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[q][nt][v] = 0.f;
-    int K = 0;
-    for (; K + 4 <= kt; K += 4) {
+        for (int v = 0; v < 4; ++v) c[nt][v] = acc[rt][0][nt][v] + acc[rt][1][nt][v];
+      const int zrow = (wa + j - x.w0) * 32 + rt * 16 + (lane >> 2);   // CTA-local row of (g)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 a = *reinterpret_cast<const uint4 *>(a_base + (size_t)(K + q) * kP2Tile);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) mma16816<T>(acc[q][nt], a, b_base[((K + q) * NT + nt) * 32]);
-      }
-    }
-    for (; K < kt; ++K) {
-      const uint4 a = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma16816<T>(acc[0][nt], a, b_base[(K * NT + nt) * 32]);
-    }
-    float c[NT][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) c[nt][v] = ((acc[0][nt][v] + acc[1][nt][v]) + acc[2][nt][v]) + acc[3][nt][v];
-    if (dt && first_job) dt[32 + warp] = (unsigned long long)(clock64() - c_job) + (c[0][0] == 1.2345e-30f ? 1 : 0);
-    const int zrow = (wa - x.w0) * 32 + j * 16 + (lane >> 2);   // CTA-local row of (g)
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      float z0, z1;
-      tile_logits<B, NT>(c, b, z0, z1);
-      if ((lane & 3) == 0) {
-        x.zbuf[b * x.zst + zrow] = z0 * inv[b];
-        x.zbuf[b * x.zst + zrow + 8] = z1 * inv[b];
+      for (int b = 0; b < B; ++b) {
+        float z0, z1;
+        tile_logits<B, NT>(c, b, z0, z1);
+        if ((lane & 3) == 0) {
+          x.zbuf[b * x.zst + zrow] = z0 * inv[b];
+          x.zbuf[b * x.zst + zrow + 8] = z1 * inv[b];
+        }
       }
     }
     __syncwarp();
     if (lane == 0) {
       // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping)
       if (j == 0) {
-        mbar_arrive(&x.hready[it % x.NS]);
-        mbar_arrive_cnt(&x.empty[it % x.NS], kConsumerWarps - 2 * nw + 1);
+        mbar_arrive(&x.hready[slot]);
+        mbar_arrive_cnt(&x.empty[slot], kConsumerWarps - nw + 1);
       } else {
-        mbar_arrive(&x.empty[it % x.NS]);
+        mbar_arrive(&x.empty[slot]);
       }
     }
     if (dt && first_job) dt[48 + warp] = globaltimer();
     first_job = false;
-  }
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
   if (dt && warp == 0) dt[3] = globaltimer();
@@ -357,7 +391,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // [8][pcap*B] phase-4 partials
   float *sg = s_part + 8 * p.pcap * B;                               // [B][kt*16] staging of g
   uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
-  __shared__ float s_gscale[B];
+  __shared__ unsigned s_gmax[B];
+  __shared__ uint32_t s_slot_pos[kMaxStages];
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
@@ -383,6 +418,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     }
     mbar_init(ids_ready, 1);
     mbar_init(p2_done, 1);
+    for (int s = 0; s < kMaxStages; ++s) s_slot_pos[s] = 0xffffffffu;
+  }
+  for (int i = tid; i < p.kt * 32; i += blockDim.x) gfrag[i] = make_uint2(0u, 0u);
+  if (tid == 0) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -399,6 +438,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       const int s = it % NS;
       const uint32_t use = it / NS;
       if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      *reinterpret_cast<volatile uint32_t *>(&s_slot_pos[s]) = it;   // the slot now belongs to position it
       if (trace && it >= trace_it0 && it - trace_it0 < 56) trace[72 + it - trace_it0] = globaltimer();
       mbar_expect_tx(&full[s], bytes);
       return stages + (size_t)s * SB;
@@ -508,6 +548,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       if (tr && tid == 0 && it - ring0 < 56) tr[16 + it - ring0] = globaltimer();
     };
     if (tid == 0) s_count = 0;
+    if (tid < B) s_gmax[tid] = 0u;
     if (tr && tid == 0) tr[0] = globaltimer();
 
     float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
@@ -600,8 +641,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
-      P2Ctx ctx{stages, full, empty, hready, zbuf, s_b2, &s_count, sg, gfrag, s_gscale, tr, NS, SB, (int)ring + st_p1,
-                st_p2, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
+      P2Ctx ctx{stages, full, empty, hready, s_slot_pos, zbuf, s_b2, &s_count, gfrag, s_gmax, tr, NS, SB,
+                (int)ring + st_p1, st_p2, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask,
+                p.uni};
       p2_phase<T, B>(ctx);
     }
     consumers_sync();
@@ -886,7 +928,7 @@ cudaError_t fused_launch_tbr(const FusedWork &w, const FusedParams &p, int CH, i
 #define PI_FL(CHV, NAV) \
   if (CH == CHV && NA == NAV) return fused_launch_t<T, B, RG, CHV, NAV>(w, p, s);
   PI_FL(1, 8) PI_FL(1, 1) PI_FL(2, 8) PI_FL(2, 1) PI_FL(3, 1) PI_FL(4, 1)
-  if (B == 1) {
+  if constexpr (B == 1) {   // wider d keeps x and y register-resident only for one token
     PI_FL(6, 1) PI_FL(8, 1)
   }
 #undef PI_FL

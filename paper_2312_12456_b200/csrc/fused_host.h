@@ -48,6 +48,7 @@ constexpr int kFusedMaxB = 2;
 constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 16384)
 constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
 constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
+constexpr int kMaxStages = 16;   // ring stages (s_slot_pos)
 
 struct FusedWork {
   bool enabled = false;
@@ -146,7 +147,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
            (size_t)kFusedMaxB * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
   };
   const size_t cap = 227 * 1024 - 1024;   // static shared memory and alignment slack
-  w.NS = (int)std::min<size_t>(200 * 1024 / sb, cap / sb);
+  w.NS = (int)std::min<size_t>({200 * 1024 / sb, cap / sb, (size_t)kMaxStages});
+  if ((size_t)w.kt * 12 * kFusedMaxB > (size_t)3 * kConsumers) return true;   // p2_phase: <= 3 entries per thread
   while (w.NS >= 2 && (size_t)w.NS * sb + extras(w.NS) > cap) --w.NS;
   if (w.NS < 2) return true;
   const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +

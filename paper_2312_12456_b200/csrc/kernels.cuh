@@ -304,6 +304,164 @@ __global__ void __launch_bounds__(256) k_down(const T *__restrict__ wdt, const T
 }
 
 // ---------------------------------------------------------------------------
+// INT4 neuron rows (PI_FFN_Q4; format DESIGN.md reading R21, oracle/quant.py O9).  Library
+// layout: one record per neuron (and per matrix) = d/2 code bytes then d/32 fp16 scales, padded
+// to 16 bytes; ReGLU up records are [gate record | up record].  w = s_g * (q - 8).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void q4_unpack8(uint32_t v, float (&f)[8]) {
+  // element k of the word = nibble k (byte b: element 2b low, 2b + 1 high); (2^23 + q) - (2^23 + 8)
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = __int_as_float(0x4B000000 | ((v >> (4 * e)) & 15u)) - 8388616.0f;
+}
+
+// a4 over INT4 rows: one warp per active neuron; lane walks 32-element groups (16 code bytes +
+// one fp16 scale per matrix); per group the integer-code dot product is scaled once.
+template <typename T, int B, bool REGLU>
+__global__ void __launch_bounds__(256) k_up_q4(const uint8_t *__restrict__ wup, int64_t rec,
+                                                const T *__restrict__ bup, const float *__restrict__ x,
+                                                const float *__restrict__ scale,
+                                                const int32_t *__restrict__ ids,
+                                                const int32_t *__restrict__ n_active,
+                                                const uint32_t *__restrict__ mask, int words, int d,
+                                                float *__restrict__ h, int hstride) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int tw = (gridDim.x * blockDim.x) >> 5;
+  const int n = *n_active;
+  const int groups = d >> 5;
+  for (int k = gw; k < n; k += tw) {
+    const int i = ids[k];
+    const uint8_t *rg = wup + (int64_t)i * (REGLU ? 2 * rec : rec);   // gate record (REGLU)
+    const uint8_t *ru = REGLU ? rg + rec : rg;                          // up record
+    float au[B], ag[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) au[b] = ag[b] = 0.f;
+    for (int g = lane; g < groups; g += 32) {
+      const Pack8 cu = ld_stream(ru + g * 16);
+      const float su = __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short *>(ru + (d >> 1)) + g)));
+      Pack8 cg;
+      float sg = 0.f;
+      if (REGLU) {
+        cg = ld_stream(rg + g * 16);
+        sg = __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short *>(rg + (d >> 1)) + g)));
+      }
+      float pu[B], pg[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) pu[b] = pg[b] = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float fu[8], fg[8];
+        q4_unpack8(cu.u[q], fu);
+        if (REGLU) q4_unpack8(cg.u[q], fg);
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          float xv[8];
+          ld_x8(x + (int64_t)b * d + g * 32 + q * 8, xv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            pu[b] = fmaf(fu[e], xv[e], pu[b]);
+            if (REGLU) pg[b] = fmaf(fg[e], xv[e], pg[b]);
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        au[b] = fmaf(su, pu[b], au[b]);
+        if (REGLU) ag[b] = fmaf(sg, pg[b], ag[b]);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      au[b] = warp_sum(au[b]);
+      if (REGLU) ag[b] = warp_sum(ag[b]);
+    }
+    if (lane < B) {
+      float a = 0.f, gt = 0.f;
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+        if (b == lane) { a = au[b]; gt = ag[b]; }
+      const float s = scale ? scale[lane] : 1.f;
+      a = a * s + (bup ? WT<T>::to_float(bup, i) : 0.f);
+      float hv = REGLU ? fmaxf(gt * s, 0.f) * a : fmaxf(a, 0.f);
+      if (mask && !((mask[(int64_t)lane * words + (i >> 5)] >> (i & 31)) & 1u)) hv = 0.f;
+      h[(int64_t)lane * hstride + k] = hv;
+    }
+  }
+}
+
+// a5 over INT4 down records: as k_down (256-column tiles x S neuron splits, fixed-order
+// reduction, integer tickets); a lane's 8 columns are one 32-bit word of codes and one scale.
+template <typename T, int B>
+__global__ void __launch_bounds__(256) k_down_q4(const uint8_t *__restrict__ wdn, int64_t rec,
+                                                  const T *__restrict__ bdown, const float *__restrict__ h,
+                                                  int hstride, const int32_t *__restrict__ ids,
+                                                  const int32_t *__restrict__ n_active, int d, int S, int tiles,
+                                                  float *__restrict__ partial, unsigned *__restrict__ tickets,
+                                                  float *__restrict__ y) {
+  extern __shared__ float red[];           // [8 warps][B][256]
+  __shared__ int last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x % tiles, s = blockIdx.x / tiles;
+  const int n = *n_active;
+  const int k0 = (int)(((int64_t)s * n) / S), k1 = (int)(((int64_t)(s + 1) * n) / S);
+  const int col = tile * 256 + lane * 8;
+  const bool valid = col < d;
+  float acc[B][8];
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[b][q] = 0.f;
+  if (valid) {
+#pragma unroll 4
+    for (int k = k0 + warp; k < k1; k += 8) {
+      const uint8_t *row = wdn + (int64_t)ids[k] * rec;
+      uint32_t cw;
+      asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(cw) : "l"(row + (col >> 1)));
+      const float sc = __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short *>(row + (d >> 1)) + (col >> 5))));
+      float wf[8];
+      q4_unpack8(cw, wf);
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const float hb = h[(int64_t)b * hstride + k] * sc;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[b][q] = fmaf(hb, wf[q], acc[b][q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) red[(warp * B + b) * 256 + lane * 8 + q] = acc[b][q];
+  __syncthreads();
+  const int c = tile * 256 + threadIdx.x;
+  if (c < d) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[(w * B + b) * 256 + threadIdx.x];
+      partial[((int64_t)s * B + b) * d + c] = v;
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(&tickets[tile], 1u) == (unsigned)(S - 1));
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (c < d) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      float v = 0.f;
+      for (int ss = 0; ss < S; ++ss) v += __ldcg(partial + ((int64_t)ss * B + b) * d + c);
+      if (bdown) v += WT<T>::to_float(bdown, c);
+      y[(int64_t)b * d + c] = v;
+    }
+  }
+  if (threadIdx.x == 0) tickets[tile] = 0u;   // re-arm for the next launch / graph replay
+}
+
+// ---------------------------------------------------------------------------
 // launchers of the per-step kernels for one weight type (instantiated in steps_inst_<T>.cu)
 // ---------------------------------------------------------------------------
 template <class F>
@@ -351,6 +509,22 @@ cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *sca
   return dispatch_batch(B, [&](auto bb) {
     constexpr int NB = decltype(bb)::value;
     const int gup = std::max(1, std::min((a.m + 7) / 8, a.num_sms * 8));
+    if (a.q4) {
+      if (a.reglu)
+        k_up_q4<T, NB, true><<<gup, 256, 0, s>>>((const uint8_t *)a.w_up, a.rec_q4, (const T *)a.b_up, x, scale, ids,
+                                                 n_active, mask, a.words, a.d, a.h, a.m);
+      else
+        k_up_q4<T, NB, false><<<gup, 256, 0, s>>>((const uint8_t *)a.w_up, a.rec_q4, (const T *)a.b_up, x, scale,
+                                                  ids, n_active, mask, a.words, a.d, a.h, a.m);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      const size_t smem = (size_t)8 * NB * 256 * 4;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(k_down_q4<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_down_q4<T, NB><<<a.tiles * a.S, 256, smem, s>>>((const uint8_t *)a.w_down, a.rec_q4, (const T *)a.b_down,
+                                                         a.h, a.m, ids, n_active, a.d, a.S, a.tiles, a.partial,
+                                                         a.tickets, y);
+      return cudaGetLastError();
+    }
     if (a.reglu)
       k_up<T, NB, true><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
                                             a.words, a.d, a.h, a.m);

@@ -17,6 +17,8 @@ struct StepArgs {
   int d, m, r, kt, words, S, tiles, num_sms;
   float t;
   bool pred_relu, reglu;
+  bool q4;            // PI_FFN_Q4: w_up / w_down are INT4 neuron records of rec_q4 bytes
+  int64_t rec_q4;
 };
 
 // kernels.cuh, instantiated per weight type in steps_inst_<T>.cu
@@ -32,6 +34,8 @@ cudaError_t launch_rms_scale(const float *x, int B, int d, float *scale, cudaStr
 cudaError_t launch_compact(const uint32_t *mask, int B, int words, int32_t *ids, int32_t *n_active, cudaStream_t s);
 cudaError_t launch_gather_rows(const void *src, const int32_t *nid, int rows, int cols, int64_t dst_stride,
                                int dst_off, void *dst, cudaStream_t s);
+cudaError_t launch_pack_q4(const void *codes, const void *scales, const int32_t *nid, int rows, int d, int64_t rec,
+                           int64_t dst_stride, int64_t dst_off, void *dst, cudaStream_t s);
 cudaError_t launch_tile_p2(const void *src, const int32_t *nid, int rows, int cols, void *dst, cudaStream_t s);
 cudaError_t launch_transpose_gather(const void *src, const int32_t *nid, int d, int m_total, int m_local,
                                     void *dst, cudaStream_t s);

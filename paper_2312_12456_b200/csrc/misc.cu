@@ -140,6 +140,28 @@ cudaError_t launch_tile_p2(const void *src, const int32_t *nid, int rows, int co
   return cudaGetLastError();
 }
 
+// INT4 neuron records: dst[k * dst_stride + dst_off + (0 .. rec)] = codes row nid[k] (d/2 bytes)
+// followed by its d/32 fp16 scales (d/16 bytes), zero padding to rec.
+__global__ void k_pack_q4(const uint8_t *__restrict__ codes, const uint8_t *__restrict__ scales,
+                          const int32_t *__restrict__ nid, int rows, int d, int64_t rec, int64_t dst_stride,
+                          int64_t dst_off, uint8_t *__restrict__ dst) {
+  const int cb = d / 2, sb = d / 16;
+  for (int k = blockIdx.y; k < rows; k += gridDim.y) {
+    const int64_t sr = nid ? nid[k] : k;
+    uint8_t *out = dst + (int64_t)k * dst_stride + dst_off;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < rec; j += (int64_t)gridDim.x * blockDim.x)
+      out[j] = j < cb ? codes[sr * cb + j] : (j < cb + sb ? scales[sr * sb + (j - cb)] : (uint8_t)0);
+  }
+}
+
+cudaError_t launch_pack_q4(const void *codes, const void *scales, const int32_t *nid, int rows, int d, int64_t rec,
+                           int64_t dst_stride, int64_t dst_off, void *dst, cudaStream_t s) {
+  dim3 grid((unsigned)std::min<int64_t>((rec + 255) / 256, 64), rows < 65535 ? rows : 65535);
+  k_pack_q4<<<grid, 256, 0, s>>>((const uint8_t *)codes, (const uint8_t *)scales, nid, rows, d, rec, dst_stride,
+                                 dst_off, (uint8_t *)dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rms_scale(const float *x, int B, int d, float *scale, cudaStream_t s) {
   k_rms_scale<<<B, 256, 0, s>>>(x, d, scale);
   return cudaGetLastError();

@@ -60,6 +60,8 @@ struct pi_layer {
   int layer_id = 0;
   int d = 0, m_local = 0, r = 0, words = 0, max_batch = 1;
   pi_dtype dtype = PI_DT_BF16;
+  pi_ffn_format ffn = PI_FFN_16;
+  int64_t rec_q4 = 0;   // PI_FFN_Q4: bytes of one neuron record (d/2 codes + d/32 fp16 scales, 16-B padded)
   pi_act act = PI_ACT_RELU;
   pi_pred_act pred_act = PI_PRED_RELU;
   uint32_t flags = 0;
@@ -158,6 +160,20 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   if (D->max_batch < 1 || D->max_batch > PI_MAX_BATCH)
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: max_batch=%d not in 1..%d", lid, D->max_batch,
                 PI_MAX_BATCH);
+  if (D->ffn_format != PI_FFN_16 && D->ffn_format != PI_FFN_Q4)
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: ffn_format %d", lid, (int)D->ffn_format);
+  const bool q4 = D->ffn_format == PI_FFN_Q4;
+  if (q4) {
+    if (D->d % 32 != 0) return fail(PI_ERR_ALIGNMENT, "layer %d: PI_FFN_Q4 needs d %% 32 == 0 (d=%d)", lid, D->d);
+    if (!D->w_up_scale || !D->w_down_scale || ((D->act == PI_ACT_REGLU) != (D->w_gate_scale != nullptr)))
+      return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: PI_FFN_Q4 needs w_up_scale, w_down_scale (and w_gate_scale iff REGLU)",
+                  lid);
+    const void *sc[] = {D->w_up_scale, D->w_gate_scale, D->w_down_scale};
+    for (const void *p : sc)
+      if (p && !aligned2(p)) return fail(PI_ERR_ALIGNMENT, "layer %d: scale pointer %p not 2-B aligned", lid, p);
+  } else if (D->w_up_scale || D->w_gate_scale || D->w_down_scale) {
+    return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: *_scale pointers are only for PI_FFN_Q4", lid);
+  }
   if (D->flags & ~(PI_FLAG_INPUT_RMSNORM | PI_FLAG_MULTI_KERNEL))
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: unknown flags 0x%x", lid, D->flags);
   if (std::isnan(D->logit_threshold))
@@ -200,6 +216,8 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   L->words = (D->m_local + 31) / 32;
   L->max_batch = D->max_batch;
   L->dtype = D->dtype;
+  L->ffn = D->ffn_format;
+  L->rec_q4 = q4 ? (((int64_t)D->d / 2 + (int64_t)D->d / 16 + 15) / 16) * 16 : 0;
   L->act = D->act;
   L->pred_act = D->pred_act;
   L->flags = D->flags;
@@ -219,8 +237,13 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
     st = dev_alloc(L, (void **)&(ptr), (size_t)(bytes), weight);           \
     if (st != PI_OK) return cleanup(st);                                   \
   } while (0)
-  ALLOC(L->w_up, (size_t)ml * d * e * (reglu ? 2 : 1), true);
-  ALLOC(L->w_down, (size_t)ml * d * e, true);
+  if (q4) {
+    ALLOC(L->w_up, (size_t)ml * L->rec_q4 * (reglu ? 2 : 1), true);
+    ALLOC(L->w_down, (size_t)ml * L->rec_q4, true);
+  } else {
+    ALLOC(L->w_up, (size_t)ml * d * e * (reglu ? 2 : 1), true);
+    ALLOC(L->w_down, (size_t)ml * d * e, true);
+  }
   if (D->b_up) ALLOC(L->b_up, (size_t)ml * e, true);
   if (D->b_down) ALLOC(L->b_down, (size_t)d * e, true);
   ALLOC(L->p_w1, (size_t)r * d * e, true);
@@ -245,7 +268,8 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   ALLOC(L->ybuf, (size_t)MB * d * 4, false);
   ALLOC(L->hx, (size_t)MB * d * 4, false);
   ALLOC(L->hy, (size_t)MB * d * 4, false);
-  if (!fused_alloc(L->fw, d, ml, r, MB, L->num_sms, reglu, [&](void **p, size_t bytes) {
+  // the fused kernel streams 16-bit rows; INT4 layers run the per-step kernels
+  if (!q4 && !fused_alloc(L->fw, d, ml, r, MB, L->num_sms, reglu, [&](void **p, size_t bytes) {
         return dev_alloc(L, p, bytes, false) == PI_OK;
       }))
     return cleanup(fail(PI_ERR_OUT_OF_MEMORY, "layer %d: fused workspace", lid));
@@ -285,7 +309,19 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
     const cudaError_t e = launch_gather_rows(src, d_nid, ml, cols, dst_stride, dst_off, dst, s);
     if (ge == cudaSuccess) ge = e;
   };
-  if (reglu) {
+  if (q4) {
+    auto pack = [&](const void *codes, const void *scales, void *dst, int64_t stride, int64_t off) {
+      const cudaError_t e2 = launch_pack_q4(codes, scales, d_nid, ml, d, L->rec_q4, stride, off, dst, s);
+      if (ge == cudaSuccess) ge = e2;
+    };
+    if (reglu) {
+      pack(D->w_gate, D->w_gate_scale, L->w_up, 2 * L->rec_q4, 0);
+      pack(D->w_up, D->w_up_scale, L->w_up, 2 * L->rec_q4, L->rec_q4);
+    } else {
+      pack(D->w_up, D->w_up_scale, L->w_up, L->rec_q4, 0);
+    }
+    pack(D->w_down, D->w_down_scale, L->w_down, L->rec_q4, 0);
+  } else if (reglu) {
     gather(D->w_gate, L->w_up, d, 2 * (int64_t)d, 0);
     gather(D->w_up, L->w_up, d, 2 * (int64_t)d, d);
   } else {
@@ -297,7 +333,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   }
   if (D->b_up) gather(D->b_up, L->b_up, 1, 1, 0);
   if (D->p_b2) gather(D->p_b2, L->p_b2, 1, 1, 0);
-  {
+  if (!q4) {
     const cudaError_t e = launch_transpose_gather(D->w_down, d_nid, d, mt, ml, L->w_down, s);
     if (ge == cudaSuccess) ge = e;
   }
@@ -466,6 +502,7 @@ extern "C" pi_status pi_layer_get_info(const pi_layer *L, pi_layer_info *info) {
   info->num_sms = L->num_sms;
   info->weight_bytes = L->weight_bytes;
   info->workspace_bytes = L->ws_bytes;
+  info->ffn_format = L->ffn;
   info->launches_per_forward =
       (!(L->flags & PI_FLAG_MULTI_KERNEL) && fused_supported(L->fw, 1)) ? 1
                                                                         : 5 + ((L->flags & PI_FLAG_INPUT_RMSNORM) ? 1 : 0);
@@ -495,6 +532,7 @@ static StepArgs step_args(const pi_layer *L) {
   a.d = L->d; a.m = L->m_local; a.r = L->r; a.kt = (L->r + 15) / 16; a.words = L->words; a.S = L->S; a.tiles = L->tiles;
   a.num_sms = L->num_sms; a.t = L->threshold;
   a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
+  a.q4 = L->ffn == PI_FFN_Q4; a.rec_q4 = L->rec_q4;
   return a;
 }
 

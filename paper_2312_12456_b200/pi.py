@@ -28,6 +28,7 @@ STATUS = {0: "PI_OK", 1: "PI_ERR_INVALID_ARGUMENT", 2: "PI_ERR_SHAPE", 3: "PI_ER
 PI_DT_F16, PI_DT_BF16 = 0, 1
 PI_ACT_RELU, PI_ACT_REGLU = 0, 1
 PI_PRED_RELU, PI_PRED_LINEAR = 0, 1
+PI_FFN_16, PI_FFN_Q4 = 0, 1
 PI_FLAG_INPUT_RMSNORM = 1
 PI_FLAG_MULTI_KERNEL = 2
 PI_MAX_BATCH = 8
@@ -55,7 +56,9 @@ class LayerDesc(ctypes.Structure):
                 ("p_b1", ctypes.c_void_p), ("p_w2", ctypes.c_void_p), ("p_b2", ctypes.c_void_p),
                 ("logit_threshold", ctypes.c_float), ("max_batch", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("neuron_freq", ctypes.POINTER(ctypes.c_float)),
-                ("hot_freq", ctypes.c_float), ("hot_cap", ctypes.c_int32)]
+                ("hot_freq", ctypes.c_float), ("hot_cap", ctypes.c_int32), ("ffn_format", ctypes.c_int),
+                ("w_up_scale", ctypes.c_void_p), ("w_gate_scale", ctypes.c_void_p),
+                ("w_down_scale", ctypes.c_void_p)]
 
 
 class LayerInfo(ctypes.Structure):
@@ -63,7 +66,8 @@ class LayerInfo(ctypes.Structure):
                 ("max_batch", ctypes.c_int32), ("mask_words", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("act", ctypes.c_int32), ("pred_act", ctypes.c_int32), ("flags", ctypes.c_uint32),
                 ("num_sms", ctypes.c_int32), ("weight_bytes", ctypes.c_int64),
-                ("workspace_bytes", ctypes.c_int64), ("launches_per_forward", ctypes.c_int32)]
+                ("workspace_bytes", ctypes.c_int64), ("launches_per_forward", ctypes.c_int32),
+                ("ffn_format", ctypes.c_int32)]
 
 
 def _load() -> ctypes.CDLL:
@@ -139,7 +143,9 @@ class Layer:
     def __init__(self, w, neuron_ids: Optional[Sequence[int]] = None, max_batch: int = 1, flags: int = 0,
                  layer_id: int = 0, threshold: Optional[float] = None, pred_act: Optional[str] = None,
                  own_b_down: bool = True, stream=None, neuron_freq=None, hot_freq: float = 0.9,
-                 hot_cap: int = 0):
+                 hot_cap: int = 0, q4=None):
+        """w: gen.LayerWeights (16-bit global tensors).  q4: optional gen.Q4Weights -- the FFN
+        then runs on INT4 neuron rows (PI_FFN_Q4); w still supplies the predictor and biases."""
         self.handle = None
         dt = w.w_up.dtype
         if dt not in _DT:
@@ -159,13 +165,19 @@ class Layer:
             assert self._freq.shape[0] == m_total
             freq_p = self._freq.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
         pa = (pred_act or getattr(w, "pred_act", "relu"))
+        if q4 is None:
+            mats = (_ptr(w.w_up), _ptr(w.w_gate), _ptr(w.w_down))
+            q4p = (PI_FFN_16, None, None, None)
+        else:
+            mats = (_ptr(q4.up_codes), _ptr(q4.gate_codes), _ptr(q4.down_codes))
+            q4p = (PI_FFN_Q4, _ptr(q4.up_scales), _ptr(q4.gate_scales), _ptr(q4.down_scales))
         desc = LayerDesc(layer_id, d, m_total, r, m_local, ids, _DT[dt],
                          PI_ACT_REGLU if w.act == "reglu" else PI_ACT_RELU,
                          PI_PRED_RELU if pa == "relu" else PI_PRED_LINEAR,
-                         _ptr(w.w_up), _ptr(w.w_gate), _ptr(w.w_down), _ptr(w.b_up),
+                         *mats, _ptr(w.b_up),
                          _ptr(w.b_down) if own_b_down else None, _ptr(w.p_w1), _ptr(w.p_b1), _ptr(w.p_w2),
                          _ptr(w.p_b2), float(thr), int(max_batch), int(flags), freq_p, float(hot_freq),
-                         int(hot_cap))
+                         int(hot_cap), *q4p)
         h = ctypes.c_void_p()
         s = _stream(stream)
         _check(_lib.pi_layer_create(ctypes.byref(desc), s, ctypes.byref(h)))
