@@ -143,7 +143,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   // partials, g staging and its B fragments; the ring gets the rest (<= 200 KB)
   auto extras = [&](int ns) {
     return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * kFusedMaxB * 4 +
-           (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
+           (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
            (size_t)kFusedMaxB * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
   };
   const size_t cap = 227 * 1024 - 1024;   // static shared memory and alignment slack
@@ -152,7 +152,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   while (w.NS >= 2 && (size_t)w.NS * sb + extras(w.NS) > cap) --w.NS;
   if (w.NS < 2) return true;
   const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                     (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
+                     (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
   w.part_off = (int)(((size_t)w.NS * sb + pre + 15) / 16 * 16);
   w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
   const int words = (m + 31) / 32;
