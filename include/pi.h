@@ -74,7 +74,10 @@ typedef enum { PI_PRED_RELU = 0, PI_PRED_LINEAR = 1 } pi_pred_act;
  * down) instead of the single fused persistent kernel (ablation / cross-check). */
 #define PI_FLAG_MULTI_KERNEL 2u
 
-#define PI_MAX_BATCH 8
+/* B <= 8: CUDA-core kernels (B <= 2 also the fused persistent kernel); 9 <= B <= 32: the
+ * batched tensor-core path (tcgen05 gathered GEMMs), which needs 16-bit FFN
+ * weights and d % 128 == 0. */
+#define PI_MAX_BATCH 32
 /* default for pi_layer_desc.hot_cap (hot neurons L2-prefetched per layer and step) */
 #define PI_DEFAULT_HOT_CAP 512
 

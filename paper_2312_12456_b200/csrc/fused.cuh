@@ -189,42 +189,12 @@ struct P2Ctx {
   uint2 *gfrag;                  // [kt][NT][32] shared B fragments
   unsigned *gmax;                // [B] shared max |g| bits (fp16 scaling), zeroed at layer start
   unsigned long long *trace;
-  int NS, SB, st_p1, st_p2, st_ring, w0, w1, m, r, kt, words, words_p2, zst;
+  int NS, SB, st_p1, st_p2, w0, w1, m, r, kt, words, words_p2, zst;
   uint32_t ring0;
   float t;
   const float *g;
-  const uint8_t *p_w2;     // this layer's fragment-major P2 (words past the ring are read from L2)
   uint32_t *mask, *uni;
 };
-
-// One warp's share of a 32-row P2 word: K tiles [k0, k1) of both row tiles, A fragments from
-// shared memory (a ring stage) or global memory (L2-prefetched), B fragments from shared memory.
-template <typename T, bool kGlobal>
-__device__ __forceinline__ void p2_mma_step(const uint8_t *a_base, const uint2 *b_base, int kt, int K,
-                                            float (&d0)[4], float (&d1)[4]) {
-  uint4 a0, a1;
-  if (kGlobal) {
-    const Pack8 p0 = ld_stream(a_base + (size_t)K * kP2Tile), p1 = ld_stream(a_base + (size_t)(kt + K) * kP2Tile);
-    a0 = make_uint4(p0.u[0], p0.u[1], p0.u[2], p0.u[3]);
-    a1 = make_uint4(p1.u[0], p1.u[1], p1.u[2], p1.u[3]);
-  } else {
-    a0 = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
-    a1 = *reinterpret_cast<const uint4 *>(a_base + (size_t)(kt + K) * kP2Tile);
-  }
-  const uint2 b = b_base[K * 32];
-  mma16816<T>(d0, a0, b);
-  mma16816<T>(d1, a1, b);
-}
-template <typename T, bool kGlobal>
-__device__ __forceinline__ void p2_word_mma(const uint8_t *a_base, const uint2 *b_base, int kt, int k0, int k1,
-                                            float (&acc)[2][2][4]) {
-  int K = k0;
-  for (; K + 1 < k1; K += 2) {   // two independent accumulator chains per row tile
-    p2_mma_step<T, kGlobal>(a_base, b_base, kt, K, acc[0][0], acc[1][0]);
-    p2_mma_step<T, kGlobal>(a_base, b_base, kt, K + 1, acc[0][1], acc[1][1]);
-  }
-  if (K < k1) p2_mma_step<T, kGlobal>(a_base, b_base, kt, K, acc[0][0], acc[1][0]);
-}
 
 template <typename T, int B>
 __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
@@ -292,67 +262,65 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   float inv[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) inv[b] = 1.f / sc[b];
-  // (2) jobs: each mask word (two 16-row tiles sharing every B fragment) is split into KS K
-  // ranges (KS = 2 when that still leaves a job per warp), round-robin over the 16 warps.  Words of
-  // the first st_ring stages come from the ring; the rest -- the predictor does not fit the ring
-  // -- are read straight from L2 (the producer prefetched them), so no job waits for a ring slot
-  // to be recycled.  A ring job first waits until the producer has acquired the slot for its
-  // position (slot_pos): after that the full barrier's parity is unambiguous.
+  // (2) jobs in ring order: job q -> stage q / J, 16-row tile and K half within it (J = 4 words_p2
+  // jobs per stage), round-robin over the 16 warps, so the first stages are worked on by many
+  // warps at once and their slots recycle quickly (the predictor does not fit the ring: the last
+  // P2 stages load into slots freed by the first).  A warp may reach a ring position whose slot
+  // still holds an older stage: it first waits until the producer has acquired the slot for this
+  // position (slot_pos), after which the full barrier's parity is unambiguous.
   const int wpp = x.words_p2, nwords = x.w1 - x.w0;
-  const int KS = (2 * nwords <= kConsumerWarps && kt >= 2) ? 2 : 1;
-  for (int job = warp; job < nwords * KS; job += kConsumerWarps) {
-    const int wl = job / KS, half = job - wl * KS;      // CTA-local word, K half
-    const int st = wl / wpp, j = wl - st * wpp;          // stage and word within it
-    const int k0 = half * kt / KS, k1 = (half + 1) * kt / KS;
-    const bool ring = st < x.st_ring;
+  const int J = 4 * wpp;                                 // jobs per full stage: 2 tiles x 2 K halves per word
+  for (int job = warp; job < x.st_p2 * J; job += kConsumerWarps) {
+    const int st = job / J, jj = job - st * J;
+    const int wl = st * wpp + (jj >> 2);                 // CTA-local word
+    if (wl >= nwords) continue;
+    const int rt = (jj >> 1) & 1, half = jj & 1;         // row tile of the word, K half
+    const int k0 = half * kt / 2, k1 = (half + 1) * kt / 2;
     const uint32_t it = x.st_p1 + st;
     const int slot = it % x.NS;
-    if (ring) {
-      while (x.slot_pos[slot] != it) __nanosleep(20);
-      mbar_wait(&x.full[slot], (it / x.NS) & 1);
-    }
-    if (x.trace && ring && j == 0 && half == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
+    while (x.slot_pos[slot] != it) __nanosleep(20);
+    mbar_wait(&x.full[slot], (it / x.NS) & 1);
+    if (x.trace && jj == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
     long long c_job = 0;
     if (dt && first_job) {
       dt[16 + warp] = globaltimer();
       c_job = clock64();
     }
-    float acc[2][2][4];   // [row tile][chain][reg]
+    float acc[2][4];   // two accumulator chains
 #pragma unroll
-    for (int rt = 0; rt < 2; ++rt)
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[rt][q][v] = 0.f;
+      for (int v = 0; v < 4; ++v) acc[q][v] = 0.f;
+    const uint8_t *a_base = x.stages + (size_t)slot * x.SB + (size_t)(2 * (jj >> 2) + rt) * kt * kP2Tile + lane * 16;
     const uint2 *b_base = x.gfrag + lane;
-    if (ring)
-      p2_word_mma<T, false>(x.stages + (size_t)slot * x.SB + (size_t)(2 * j) * kt * kP2Tile + lane * 16, b_base, kt, k0,
-                            k1, acc);
-    else
-      p2_word_mma<T, true>(x.p_w2 + (size_t)(2 * (x.w0 + wl)) * kt * kP2Tile + lane * 16, b_base, kt, k0, k1, acc);
-    if (dt && first_job) dt[32 + warp] = (unsigned long long)(clock64() - c_job) + (acc[0][0][0] == 1.2345e-30f ? 1 : 0);
+    int K = k0;
+    for (; K + 1 < k1; K += 2) {
+      const uint4 a0 = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
+      const uint4 a1 = *reinterpret_cast<const uint4 *>(a_base + (size_t)(K + 1) * kP2Tile);
+      mma16816<T>(acc[0], a0, b_base[K * 32]);
+      mma16816<T>(acc[1], a1, b_base[(K + 1) * 32]);
+    }
+    if (K < k1) mma16816<T>(acc[0], *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile), b_base[K * 32]);
+    if (dt && first_job) dt[32 + warp] = (unsigned long long)(clock64() - c_job) + (acc[0][0] == 1.2345e-30f ? 1 : 0);
+    float c[1][4];
 #pragma unroll
-    for (int rt = 0; rt < 2; ++rt) {
-      float c[1][4];
+    for (int v = 0; v < 4; ++v) c[0][v] = acc[0][v] + acc[1][v];
+    const int zrow = wl * 32 + rt * 16 + (lane >> 2);   // CTA-local row of (g)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) c[0][v] = acc[rt][0][v] + acc[rt][1][v];
-      const int zrow = wl * 32 + rt * 16 + (lane >> 2);   // CTA-local row of (g)
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        float z0, z1;
-        tile_logits<B, 1>(c, b, z0, z1);
-        if ((lane & 3) == 0) {
-          float *zb = x.zbuf + (half * B + b) * x.zst;     // [K half][token][row]
-          zb[zrow] = z0 * inv[b];
-          zb[zrow + 8] = z1 * inv[b];
-        }
+    for (int b = 0; b < B; ++b) {
+      float z0, z1;
+      tile_logits<B, 1>(c, b, z0, z1);
+      if ((lane & 3) == 0) {
+        float *zb = x.zbuf + (half * B + b) * x.zst;     // [K half][token][row]
+        zb[zrow] = z0 * inv[b];
+        zb[zrow + 8] = z1 * inv[b];
       }
     }
     __syncwarp();
-    if (ring && lane == 0) {
+    if (lane == 0) {
       // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping)
-      const int jobs_here = (min(x.w1, x.w0 + (st + 1) * wpp) - (x.w0 + st * wpp)) * KS;
-      if (j == 0 && half == 0) {
+      const int jobs_here = 4 * (min(nwords, (st + 1) * wpp) - st * wpp);
+      if (jj == 0) {
         mbar_arrive(&x.hready[slot]);
         mbar_arrive_cnt(&x.empty[slot], kConsumerWarps - jobs_here + 1);
       } else {
@@ -361,9 +329,6 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     }
     if (dt && first_job) dt[48 + warp] = globaltimer();
     first_job = false;
-  }
-  if (KS == 1) {   // the ballots add the two K halves
-    for (int i = tid; i < B * x.zst; i += kConsumers) x.zbuf[B * x.zst + i] = 0.f;
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
   if (dt && warp == 0) dt[3] = globaltimer();
@@ -436,7 +401,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   const int st_p1 = (n_p1 + RP1 - 1) / RP1;
   const int w0 = (int)(((int64_t)c * p.words) / P), w1 = (int)(((int64_t)(c + 1) * p.words) / P);
   const int st_p2 = (w1 - w0 + p.words_p2 - 1) / p.words_p2;
-  // P2 stages that go through the ring (the rest are read from L2 by the consumers)
+  // P2 stages that fit the ring at the layer start (the rest stream in as slots recycle; their
+  // rows are L2-prefetched during the previous layer's tail)
   const int st_p2_ring = min(st_p2, max(0, NS - st_p1));
   const size_t row_up = (size_t)d * 2 * (REGLU ? 2 : 1);  // bytes of one up (gate|up) row
   const size_t row_dn = (size_t)d * 2;
@@ -526,7 +492,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           bulk_g2s(dst + (size_t)k * row_dn, lw.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
         }
       }
-      for (int st = 0; st < st_p2_ring; ++st, ++it) {  // phase 2: P2 words [w0, ...) that fit the ring
+      for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 words [w0, w1), contiguous
+        if (st == st_p2_ring) prefetch_tail(NS);
         prefetch_tail(st_p1 + st);
         const int wa = w0 + st * p.words_p2, wb = min(w1, wa + p.words_p2);
         const int ra = wa * 32, rb = wb * 32;   // whole (zero-padded) words
@@ -681,8 +648,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
       P2Ctx ctx{stages, full, empty, hready, s_slot_pos, zbuf, s_b2, &s_count, gfrag, s_gmax, tr, NS, SB,
-                (int)ring + st_p1, st_p2, st_p2_ring, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t,
-                p.g, lw.p_w2, p.mask, p.uni};
+                (int)ring + st_p1, st_p2, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g,
+                p.mask, p.uni};
       p2_phase<T, B>(ctx);
     }
     consumers_sync();
@@ -697,7 +664,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     // One L2 round trip: all consumer threads stage the P counts, the union words and (B > 1)
     // the per-token words into the ring slot the first FFN stage will use -- free now: every
     // predictor stage has been consumed and the producer waits for ids_ready before reusing it.
-    const uint32_t it_ffn = ring + st_p1 + st_p2_ring;
+    const uint32_t it_ffn = ring + st_p1 + st_p2;
     uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
     uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (B > 1)
     int *c_cnt = reinterpret_cast<int *>(c_msk + (B > 1 ? B * p.words : 0));   // [P]

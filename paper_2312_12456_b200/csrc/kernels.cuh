@@ -10,6 +10,7 @@
 #include <type_traits>
 
 #include "launch.h"
+#include "tc.cuh"
 
 namespace pi {
 
@@ -21,7 +22,7 @@ template <typename T, int B, bool PRED_RELU>
 __global__ void __launch_bounds__(256) k_predict1(const T *__restrict__ p1, const T *__restrict__ b1,
                                                    const float *__restrict__ x,
                                                    const float *__restrict__ scale, int r, int d,
-                                                   float *__restrict__ g) {
+                                                   float *__restrict__ g, int nb) {
   constexpr int KS = 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 2 + warp / KS;
@@ -40,6 +41,7 @@ __global__ void __launch_bounds__(256) k_predict1(const T *__restrict__ p1, cons
       WT<T>::unpack(pw, wf);
 #pragma unroll
       for (int b = 0; b < B; ++b) {
+        if (B > 8 && b >= nb) break;
         float xv[8];
         ld_x8(x + (int64_t)b * d + c * 8, xv);
 #pragma unroll
@@ -57,7 +59,7 @@ __global__ void __launch_bounds__(256) k_predict1(const T *__restrict__ p1, cons
   if (threadIdx.x < 2 * B) {
     const int rr = threadIdx.x / B, b = threadIdx.x % B;
     const int orow = blockIdx.x * 2 + rr;
-    if (orow < r) {
+    if (orow < r && b < nb) {
       float u = 0.f;
 #pragma unroll
       for (int p = 0; p < KS; ++p) u += red[rr * KS + p][b];
@@ -79,8 +81,9 @@ template <typename T, int B>
 __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, const T *__restrict__ b2,
                                                    const float *__restrict__ g, float t, int m, int r, int kt,
                                                    int words, uint32_t *__restrict__ mask,
-                                                   float *__restrict__ logits) {
+                                                   float *__restrict__ logits, int nb) {
   constexpr int NT = (3 * B + 7) / 8;
+  constexpr int NC = NT >= 3 ? 1 : (NT == 2 ? 2 : 4);   // independent accumulator chains
   extern __shared__ __align__(16) float p2smem[];
   const int ldg = kt * 16;
   float *gs = p2smem;                                          // [B][ldg]
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, con
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < B * ldg; i += blockDim.x) {
     const int b = i / ldg, k = i - b * ldg;
-    gs[i] = (k < r) ? g[(int64_t)b * r + k] : 0.f;
+    gs[i] = (k < r && b < nb) ? g[(int64_t)b * r + k] : 0.f;
   }
   __syncthreads();
   if (warp < B) {
@@ -107,20 +110,20 @@ __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, con
   const int R = blockIdx.x * 8 + warp;   // global row tile
   if (R * 16 < words * 32) {
     const uint8_t *a_base = reinterpret_cast<const uint8_t *>(p2t) + (size_t)R * kt * kP2Tile + lane * 16;
-    float acc[4][NT][4];
+    float acc[NC][NT][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < NC; ++q)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[q][nt][v] = 0.f;
     int K = 0;
-    for (; K + 4 <= kt; K += 4) {
-      Pack8 a[4];
+    for (; K + NC <= kt; K += NC) {
+      Pack8 a[NC];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) a[q] = ld_stream(a_base + (size_t)(K + q) * kP2Tile);
+      for (int q = 0; q < NC; ++q) a[q] = ld_stream(a_base + (size_t)(K + q) * kP2Tile);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < NC; ++q)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
           mma16816<T>(acc[q][nt], make_uint4(a[q].u[0], a[q].u[1], a[q].u[2], a[q].u[3]),
@@ -136,7 +139,12 @@ __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, con
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) c[nt][v] = ((acc[0][nt][v] + acc[1][nt][v]) + acc[2][nt][v]) + acc[3][nt][v];
+      for (int v = 0; v < 4; ++v) {
+        float s = acc[0][nt][v];
+#pragma unroll
+        for (int q = 1; q < NC; ++q) s += acc[q][nt][v];
+        c[nt][v] = s;
+      }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       float z0, z1;
@@ -155,6 +163,7 @@ __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, con
     const int i = word * 32 + lane;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
+      if (b >= nb) break;
       float z = __int_as_float(0x7fc00000);          // NaN: never active
       if (i < m) z = zb[b * 128 + warp * 32 + lane] + (b2 ? WT<T>::to_float(b2, i) : 0.f);
       const uint32_t bits = __ballot_sync(0xffffffffu, z > t);
@@ -465,7 +474,7 @@ __global__ void __launch_bounds__(256) k_down_q4(const uint8_t *__restrict__ wdn
 // launchers of the per-step kernels for one weight type (instantiated in steps_inst_<T>.cu)
 // ---------------------------------------------------------------------------
 template <class F>
-static cudaError_t dispatch_batch(int B, F &&f) {
+static cudaError_t dispatch_small(int B, F &&f) {
   switch (B) {
     case 1: return f(std::integral_constant<int, 1>{});
     case 2: return f(std::integral_constant<int, 2>{});
@@ -478,6 +487,12 @@ static cudaError_t dispatch_batch(int B, F &&f) {
   }
   return cudaErrorInvalidValue;
 }
+template <class F>
+static cudaError_t dispatch_batch(int B, F &&f) {
+  if (B > 8 && B <= 16) return f(std::integral_constant<int, 16>{});   // batched (f2): tokens padded
+  if (B > 16 && B <= 32) return f(std::integral_constant<int, 32>{});
+  return dispatch_small(B, f);
+}
 
 template <typename T>
 cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float *scale, uint32_t *mask,
@@ -486,9 +501,9 @@ cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float 
     constexpr int NB = decltype(bb)::value;
     const int g1 = (a.r + 1) / 2;
     if (a.pred_relu)
-      k_predict1<T, NB, true><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g);
+      k_predict1<T, NB, true><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g, B);
     else
-      k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g);
+      k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g, B);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     constexpr int NT = (3 * NB + 7) / 8;
@@ -498,15 +513,54 @@ cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float 
       if (e != cudaSuccess) return e;
     }
     k_predict2<T, NB><<<(a.words + 3) / 4, 256, smem, s>>>((const T *)a.p_w2, (const T *)a.p_b2, a.g, a.t, a.m,
-                                                           a.r, a.kt, a.words, mask, logits);
+                                                           a.r, a.kt, a.words, mask, logits, B);
     return cudaGetLastError();
   });
+}
+
+// batched decode on the tensor cores (B = 9..32, row f2): x splits -> k_up_tc -> k_down_tc
+template <typename T, int BMAX>
+cudaError_t steps_ffn_tc(const StepArgs &a, const float *x, int B, const float *scale, const int32_t *ids,
+                         const int32_t *n_active, const uint32_t *mask, float *y, cudaStream_t s) {
+  constexpr int N = 3 * BMAX;
+  k_split_x<T, BMAX><<<a.num_sms * 4, 256, 0, s>>>(x, B, a.d, a.x3);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int up_smem = kTcStages * ((a.reglu ? 2 : 1) * 128 * kTcKB * 2 + N * 128) + 256;
+  const int dn_smem = kTcStages * (128 * kTcKB * 2 + N * 128) + 256;
+  if (a.reglu) {
+    e = cudaFuncSetAttribute(k_up_tc<T, BMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, up_smem);
+    if (e != cudaSuccess) return e;
+    k_up_tc<T, BMAX, true><<<a.num_sms, kTcThreads, up_smem, s>>>((const uint8_t *)a.w_up, (const T *)a.b_up, a.x3,
+                                                                  scale, ids, n_active, mask, a.words, a.d, B, a.h,
+                                                                  a.m, a.h3);
+  } else {
+    e = cudaFuncSetAttribute(k_up_tc<T, BMAX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, up_smem);
+    if (e != cudaSuccess) return e;
+    k_up_tc<T, BMAX, false><<<a.num_sms, kTcThreads, up_smem, s>>>((const uint8_t *)a.w_up, (const T *)a.b_up, a.x3,
+                                                                   scale, ids, n_active, mask, a.words, a.d, B, a.h,
+                                                                   a.m, a.h3);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_down_tc<T, BMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, dn_smem);
+  if (e != cudaSuccess) return e;
+  const int tiles = a.d / 128;
+  k_down_tc<T, BMAX><<<std::min(a.num_sms, tiles * a.S_tc), kTcThreads, dn_smem, s>>>(
+      (const uint8_t *)a.w_down, (const T *)a.b_down, a.h3, ids, n_active, a.d, B, a.S_tc, a.partial_tc,
+      a.tickets_tc, y);
+  return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *scale, const int32_t *ids,
                       const int32_t *n_active, const uint32_t *mask, float *y, cudaStream_t s) {
-  return dispatch_batch(B, [&](auto bb) {
+  if (B > 8 && !a.q4) {
+    if (!a.x3) return cudaErrorNotSupported;
+    return B <= 16 ? steps_ffn_tc<T, 16>(a, x, B, scale, ids, n_active, mask, y, s)
+                   : steps_ffn_tc<T, 32>(a, x, B, scale, ids, n_active, mask, y, s);
+  }
+  return dispatch_small(B, [&](auto bb) {
     constexpr int NB = decltype(bb)::value;
     const int gup = std::max(1, std::min((a.m + 7) / 8, a.num_sms * 8));
     if (a.q4) {

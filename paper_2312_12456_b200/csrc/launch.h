@@ -19,6 +19,11 @@ struct StepArgs {
   bool pred_relu, reglu;
   bool q4;            // PI_FFN_Q4: w_up / w_down are INT4 neuron records of rec_q4 bytes
   int64_t rec_q4;
+  // batched tensor-core path (B = 9..32, tc.cuh); x3 == NULL when the layer does not support it
+  uint16_t *x3, *h3;
+  float *partial_tc;
+  unsigned *tickets_tc;
+  int S_tc;
 };
 
 // kernels.cuh, instantiated per weight type in steps_inst_<T>.cu

@@ -82,6 +82,11 @@ struct pi_layer {
   int32_t *n_active = nullptr;
   float *xbuf = nullptr, *ybuf = nullptr;  // [max_batch, d] each (stack ping-pong)
   float *hx = nullptr, *hy = nullptr;      // [max_batch, d] each (host-buffer entry points)
+  // batched tensor-core path (max_batch > 8): activation splits, partials, tickets (tc.cuh)
+  uint16_t *x3 = nullptr, *h3 = nullptr;
+  float *partial_tc = nullptr;
+  unsigned *tickets_tc = nullptr;
+  int S_tc = 0;
   int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons, hottest first
   int n_hot = 0, hot_cap = 0;
   FusedWork fw{};             // fused-kernel workspace
@@ -176,6 +181,9 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   }
   if (D->flags & ~(PI_FLAG_INPUT_RMSNORM | PI_FLAG_MULTI_KERNEL))
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: unknown flags 0x%x", lid, D->flags);
+  if (D->max_batch > 8 && (q4 || D->d % 128 != 0))
+    return fail(PI_ERR_UNSUPPORTED, "layer %d: max_batch=%d > 8 (the tensor-core batched path) needs 16-bit FFN "
+                "weights and d %% 128 == 0 (d=%d)", lid, D->max_batch, D->d);
   if (std::isnan(D->logit_threshold))
     return fail(PI_ERR_INVALID_ARGUMENT, "layer %d: logit_threshold is NaN", lid);
   if (!D->w_up || !D->w_down || !D->p_w1 || !D->p_w2)
@@ -268,6 +276,14 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   ALLOC(L->ybuf, (size_t)MB * d * 4, false);
   ALLOC(L->hx, (size_t)MB * d * 4, false);
   ALLOC(L->hy, (size_t)MB * d * 4, false);
+  if (MB > 8) {
+    const int bmax = MB <= 16 ? 16 : 32, N = 3 * bmax;
+    L->S_tc = std::max(1, std::min(8, L->num_sms / std::max(1, d / 128)));
+    ALLOC(L->x3, (size_t)d * N * 2, false);
+    ALLOC(L->h3, (size_t)((ml + 63) / 64) * 64 * N * 2, false);
+    ALLOC(L->partial_tc, (size_t)L->S_tc * bmax * d * 4, false);
+    ALLOC(L->tickets_tc, (size_t)(d / 128) * 4, false);
+  }
   // the fused kernel streams 16-bit rows; INT4 layers run the per-step kernels
   if (!q4 && !fused_alloc(L->fw, d, ml, r, MB, L->num_sms, reglu, [&](void **p, size_t bytes) {
         return dev_alloc(L, p, bytes, false) == PI_OK;
@@ -341,6 +357,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   if (D->p_b1) cudaMemcpyAsync(L->p_b1, D->p_b1, (size_t)r * e, cudaMemcpyDeviceToDevice, s);
   if (D->b_down) cudaMemcpyAsync(L->b_down, D->b_down, (size_t)d * e, cudaMemcpyDeviceToDevice, s);
   cudaMemsetAsync(L->tickets, 0, (size_t)L->tiles * 4, s);
+  if (L->tickets_tc) cudaMemsetAsync(L->tickets_tc, 0, (size_t)(d / 128) * 4, s);
   cudaMemsetAsync(L->n_active, 0, 16, s);
   fused_init(L->fw, s);
   cudaError_t ce = cudaGetLastError();
@@ -533,6 +550,7 @@ static StepArgs step_args(const pi_layer *L) {
   a.num_sms = L->num_sms; a.t = L->threshold;
   a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
   a.q4 = L->ffn == PI_FFN_Q4; a.rec_q4 = L->rec_q4;
+  a.x3 = L->x3; a.h3 = L->h3; a.partial_tc = L->partial_tc; a.tickets_tc = L->tickets_tc; a.S_tc = L->S_tc;
   return a;
 }
 

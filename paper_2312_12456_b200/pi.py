@@ -31,7 +31,7 @@ PI_PRED_RELU, PI_PRED_LINEAR = 0, 1
 PI_FFN_16, PI_FFN_Q4 = 0, 1
 PI_FLAG_INPUT_RMSNORM = 1
 PI_FLAG_MULTI_KERNEL = 2
-PI_MAX_BATCH = 8
+PI_MAX_BATCH = 32
 
 EXPORTS = ("pi_version", "pi_last_error", "pi_layer_create", "pi_layer_destroy", "pi_layer_get_info",
            "pi_predict", "pi_compact", "pi_sparse_ffn", "pi_layer_forward", "pi_layer_forward_host",

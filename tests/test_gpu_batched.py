@@ -1,0 +1,129 @@
+"""GPU parity of the batched-decode tensor-core path (B = 9..32, row f2: tcgen05 gathered GEMMs,
+csrc/tc.cuh) against the oracle: integer-exact layers bit for bit, random layers within the
+north_star tolerance (rel-L2 <= 1e-3, internal gate 1e-5) with the oracle fed the GPU's own ids
+and mask bits (per-token semantics, reading R9), batch invariance against the B = 1 path, and one
+full-size c3 layer (ReGLU) at B = 16 and 32.  "Batching Inference"."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import ffn as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+GATE = 1e-5
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2312_12456_b200 import gen, pi
+    torch.cuda.set_device(0)
+    return gen, pi
+
+
+def f(t):
+    return None if t is None else t.float().cpu().numpy()
+
+
+def _run(L, x):
+    B = x.shape[0]
+    y = torch.full((B, L.d), float("nan"), device="cuda")
+    mask = L.new_mask(B)
+    ids = L.new_ids()
+    n = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    L.forward(x, y, mask, ids, n)
+    torch.cuda.synchronize()
+    nn = int(n.item())
+    return y.cpu().numpy(), O.unpack_mask(mask.cpu().numpy().view(np.uint32), L.m_local), ids[:nn].cpu().numpy()
+
+
+def _check(w, x, y, gm, ids, norm):
+    xo = f(x).astype(np.float64)
+    if norm:
+        xo = O.rms_normalize(xo)
+    om, z = O.predict(xo, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), w.threshold, w.pred_act)
+    assert ((gm == om) | O.near_threshold(z, w.threshold)).all()
+    assert (ids == O.compact(gm)).all()
+    yo = O.sparse_ffn(xo, ids, gm, f(w.w_up), f(w.b_up), f(w.w_gate), f(w.w_down), f(w.b_down), w.act)
+    return O.rel_l2(y, yo), yo
+
+
+@pytest.mark.parametrize("B", [9, 16, 32])
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_integer_layer_batched_bitwise(env, B, dtype):
+    gen, pi = env
+    d, m, r = 256, 1000, 64
+    w = gen.make_int_layer(d, m, r, "relu", seed=d + m + B, dtype=dtype, device="cuda")
+    L = pi.Layer(w, max_batch=32)
+    x = gen.int_tokens(B, d, "relu", seed=B).cuda()
+    y, gm, ids = _run(L, x)
+    xo = f(x).astype(np.float64)
+    om, z = O.predict(xo, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), 0.5)
+    assert (gm == om).all()
+    assert (ids == O.compact(om)).all()
+    yo = O.sparse_ffn(xo, ids, om, f(w.w_up), f(w.b_up), None, f(w.w_down), f(w.b_down), "relu")
+    assert (y == yo).all()
+
+
+@pytest.mark.parametrize("name,dims", [("c3", (5120, 3000, 320)), ("c4", (8192, 4096, 512)),
+                                       ("c2", (4096, 2500, 256)), ("c1", (768, 3072, 64))])
+@pytest.mark.parametrize("B", [12, 16, 32])
+def test_random_layers_batched(env, name, dims, B):
+    gen, pi = env
+    cfg = gen.CONFIGS[name]
+    d, m, r = dims
+    w = gen.make_layer(cfg, seed=5, device="cuda", d=d, m=m, r=r)
+    flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
+    L = pi.Layer(w, max_batch=32, flags=flags)
+    x = gen.tokens(B, d, seed=9, device="cuda") * (3.0 if cfg.rmsnorm else 1.0)
+    y, gm, ids = _run(L, x)
+    err, _ = _check(w, x, y, gm, ids, cfg.rmsnorm)
+    assert err <= TOL and err <= GATE, err
+
+
+def test_batched_equals_single_token_path(env):
+    """Batch invariance (R9): each token of a B = 20 batch equals that token run alone (B = 1 takes
+    the CUDA-core kernels), and repeated runs are bitwise identical (fixed reduction order)."""
+    gen, pi = env
+    cfg = gen.CONFIGS["c3"]
+    w = gen.make_layer(cfg, seed=4, device="cuda", d=1024, m=2000, r=64)
+    L = pi.Layer(w, max_batch=32, flags=pi.PI_FLAG_INPUT_RMSNORM)
+    x = gen.tokens(20, 1024, device="cuda")
+    y, gm, ids = _run(L, x)
+    for b in (0, 7, 19):
+        yb, gmb, _ = _run(L, x[b:b + 1].contiguous())
+        assert (gmb[0] == gm[b]).all()
+        assert O.rel_l2(yb[0], y[b]) <= GATE
+    for _ in range(5):
+        assert (_run(L, x)[0] == y).all()
+
+
+def test_empty_and_full_masks_batched(env):
+    gen, pi = env
+    cfg = gen.CONFIGS["c1"]
+    w = gen.make_layer(cfg, seed=1, device="cuda", d=512, m=700, r=32)
+    x = gen.tokens(16, 512, device="cuda")
+    L = pi.Layer(w, max_batch=16, threshold=float("inf"))
+    y, gm, ids = _run(L, x)
+    assert len(ids) == 0 and (y == np.tile(f(w.b_down), (16, 1))).all()
+    L = pi.Layer(w, max_batch=16, threshold=float("-inf"))
+    y, gm, ids = _run(L, x)
+    assert len(ids) == 700
+    yd = O.dense_ffn(f(x), f(w.w_up), f(w.b_up), None, f(w.w_down), f(w.b_down))
+    assert O.rel_l2(y, yd) <= GATE
+
+
+@pytest.mark.parametrize("B", [16, 32])
+def test_full_size_c3_layer_batched(env, B):
+    gen, pi = env
+    cfg = gen.CONFIGS["c3"]
+    w = gen.make_layer(cfg, seed=0, device="cuda")
+    L = pi.Layer(w, max_batch=B, flags=pi.PI_FLAG_INPUT_RMSNORM)
+    x = gen.tokens(B, cfg.d, seed=1, device="cuda")
+    y, gm, ids = _run(L, x)
+    err, _ = _check(w, x, y, gm, ids, True)
+    assert err <= GATE, err
+    assert 0.3 < len(ids) / cfg.m < 0.9      # the union grows with B
