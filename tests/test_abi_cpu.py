@@ -99,7 +99,13 @@ def _create_status(pi, desc):
     (dict(w_up=0x10004), 4),                # misaligned weight pointer
     (dict(m_local=64), 2),                  # neuron_ids NULL requires m_local == m_total
     (dict(m_local=256), 2),
-    (dict(max_batch=9), 1),
+    (dict(max_batch=33), 1),                # > PI_MAX_BATCH
+    (dict(max_batch=9), 5),                 # tensor-core batched path needs d % 128 == 0 -> UNSUPPORTED
+    (dict(ffn_format=7), 1),                # unknown FFN format
+    (dict(ffn_format=1), 1),                # PI_FFN_Q4 without scales
+    (dict(ffn_format=1, d=40, w_up_scale=0x50000, w_down_scale=0x60000), 4),   # Q4 needs d % 32 == 0
+    (dict(w_up_scale=0x50000), 1),          # scales only for Q4
+    (dict(ffn_format=1, max_batch=16, d=128, w_up_scale=0x50000, w_down_scale=0x60000), 5),  # Q4 is B <= 8
     (dict(max_batch=0), 1),
     (dict(act=1), 1),                       # ReGLU without gate
     (dict(dtype=5), 5),
