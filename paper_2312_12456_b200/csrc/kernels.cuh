@@ -96,12 +96,12 @@ __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, con
     gs[i] = (k < r && b < nb) ? g[(int64_t)b * r + k] : 0.f;
   }
   __syncthreads();
-  if (warp < B) {
+  for (int b = warp; b < B; b += 8) {   // per-token range scale (8 warps, up to 32 tokens)
     float mx = 0.f;
-    for (int k = lane; k < r; k += 32) mx = fmaxf(mx, fabsf(gs[warp * ldg + k]));
+    for (int k = lane; k < r; k += 32) mx = fmaxf(mx, fabsf(gs[b * ldg + k]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) gscale[warp] = g_scale<T>(mx);
+    if (lane == 0) gscale[b] = g_scale<T>(mx);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kt * NT * 32; e += blockDim.x)
