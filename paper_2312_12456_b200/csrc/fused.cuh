@@ -189,7 +189,7 @@ struct P2Ctx {
   uint2 *gfrag;                  // [kt][NT][32] shared B fragments
   unsigned *gmax;                // [B] shared max |g| bits (fp16 scaling), zeroed at layer start
   unsigned long long *trace;
-  int NS, SB, st_p1, st_p2, w0, w1, m, r, kt, kp, words, words_p2, zst;
+  int NS, SB, st_p1, st_p2, w0, w1, m, r, kt, words, words_p2, zst;
   uint32_t ring0;
   float t;
   const float *g;
@@ -262,29 +262,25 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   float inv[B];
 #pragma unroll
   for (int b = 0; b < B; ++b) inv[b] = 1.f / sc[b];
-  // (2) jobs: (16-row tile t in ring order) x (K part p of KP); job q -> warp q % 16, so a warp
-  // always works on the same K part and keeps that part's B fragments in registers (no shared
-  // reloads; the phase streams each P2 byte from shared memory once).  Partial logits go to
-  // zbuf[p], summed in order p = 0..KP-1 by the ballots.  A warp may reach a ring position whose
-  // slot still holds an older stage: it first waits until the producer has acquired the slot for
-  // this position (slot_pos), after which the full barrier's parity is unambiguous.
-  const int wpp = x.words_p2, nwords = x.w1 - x.w0, KP = x.kp;
-  const int p = warp % KP;
-  const int kp0 = p * kt / KP, ntp = (p + 1) * kt / KP - kp0;   // <= kMaxKPT tiles
-  uint2 bf[kMaxKPT];
-#pragma unroll
-  for (int i = 0; i < kMaxKPT; ++i) bf[i] = (i < ntp) ? x.gfrag[(kp0 + i) * 32 + lane] : make_uint2(0u, 0u);
-  const int RT = 2 * nwords;
-  for (int job = warp; job < RT * KP; job += kConsumerWarps) {
-    const int t = job / KP;
-    const int wl = t >> 1, rt = t & 1;                 // CTA-local word, its row tile
-    const int st = wl / wpp, j = wl - st * wpp;        // stage, word within it
+  // (2) jobs in ring order: job q -> stage q / J, 16-row tile and K half within it (J = 4 words_p2
+  // jobs per stage), round-robin over the 16 warps, so the first stages are worked on by many
+  // warps at once and their slots recycle quickly (the predictor does not fit the ring: the last
+  // P2 stages load into slots freed by the first).  A warp may reach a ring position whose slot
+  // still holds an older stage: it first waits until the producer has acquired the slot for this
+  // position (slot_pos), after which the full barrier's parity is unambiguous.
+  const int wpp = x.words_p2, nwords = x.w1 - x.w0;
+  const int J = 4 * wpp;                                 // jobs per full stage: 2 tiles x 2 K halves per word
+  for (int job = warp; job < x.st_p2 * J; job += kConsumerWarps) {
+    const int st = job / J, jj = job - st * J;
+    const int wl = st * wpp + (jj >> 2);                 // CTA-local word
+    if (wl >= nwords) continue;
+    const int rt = (jj >> 1) & 1, half = jj & 1;         // row tile of the word, K half
+    const int k0 = half * kt / 2, k1 = (half + 1) * kt / 2;
     const uint32_t it = x.st_p1 + st;
     const int slot = it % x.NS;
     while (x.slot_pos[slot] != it) __nanosleep(20);
     mbar_wait(&x.full[slot], (it / x.NS) & 1);
-    const int t_first = 2 * st * wpp;                  // first row tile of this stage
-    if (x.trace && t == t_first && p == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
+    if (x.trace && jj == 0 && lane == 0 && it - x.ring0 < 56) x.trace[16 + it - x.ring0] = globaltimer();
     long long c_job = 0;
     if (dt && first_job) {
       dt[16 + warp] = globaltimer();
@@ -295,11 +291,16 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[q][v] = 0.f;
-    const uint8_t *a_base =
-        x.stages + (size_t)slot * x.SB + ((size_t)(2 * j + rt) * kt + kp0) * kP2Tile + lane * 16;
-#pragma unroll
-    for (int i = 0; i < kMaxKPT; ++i)
-      if (i < ntp) mma16816<T>(acc[i & 1], *reinterpret_cast<const uint4 *>(a_base + (size_t)i * kP2Tile), bf[i]);
+    const uint8_t *a_base = x.stages + (size_t)slot * x.SB + (size_t)(2 * (jj >> 2) + rt) * kt * kP2Tile + lane * 16;
+    const uint2 *b_base = x.gfrag + lane;
+    int K = k0;
+    for (; K + 1 < k1; K += 2) {
+      const uint4 a0 = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
+      const uint4 a1 = *reinterpret_cast<const uint4 *>(a_base + (size_t)(K + 1) * kP2Tile);
+      mma16816<T>(acc[0], a0, b_base[K * 32]);
+      mma16816<T>(acc[1], a1, b_base[(K + 1) * 32]);
+    }
+    if (K < k1) mma16816<T>(acc[0], *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile), b_base[K * 32]);
     if (dt && first_job) dt[32 + warp] = (unsigned long long)(clock64() - c_job) + (acc[0][0] == 1.2345e-30f ? 1 : 0);
     float c[1][4];
 #pragma unroll
@@ -310,24 +311,21 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       float z0, z1;
       tile_logits<B, 1>(c, b, z0, z1);
       if ((lane & 3) == 0) {
-        float *zb = x.zbuf + (p * B + b) * x.zst;      // [K part][token][row]
+        float *zb = x.zbuf + (half * B + b) * x.zst;     // [K half][token][row]
         zb[zrow] = z0 * inv[b];
         zb[zrow + 8] = z1 * inv[b];
       }
     }
     __syncwarp();
-    // ring bookkeeping: every use of a slot gets kConsumerWarps arrivals on `empty` and one on
-    // `hready`.  Each warp that worked on the stage arrives once, after its last job there; the
-    // stage's first job also arrives for the warps that had no job in it.
-    const int t_end = 2 * min(nwords, (st + 1) * wpp);
-    const int jobs_here = (t_end - t_first) * KP;
-    const bool last_here = (job + kConsumerWarps) / KP >= t_end || job + kConsumerWarps >= RT * KP;
     if (lane == 0) {
-      if (t == t_first && p == 0) {
+      // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping)
+      const int jobs_here = 4 * (min(nwords, (st + 1) * wpp) - st * wpp);
+      if (jj == 0) {
         mbar_arrive(&x.hready[slot]);
-        if (jobs_here < kConsumerWarps) mbar_arrive_cnt(&x.empty[slot], kConsumerWarps - jobs_here);
+        mbar_arrive_cnt(&x.empty[slot], kConsumerWarps - jobs_here + 1);
+      } else {
+        mbar_arrive(&x.empty[slot]);
       }
-      if (last_here) mbar_arrive(&x.empty[slot]);
     }
     if (dt && first_job) dt[48 + warp] = globaltimer();
     first_job = false;
@@ -342,12 +340,8 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     uint32_t u = 0;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      float z = __int_as_float(0x7fc00000);
-      if (valid) {
-        z = x.zbuf[b * x.zst + rl];
-        for (int q = 1; q < x.kp; ++q) z += x.zbuf[(q * B + b) * x.zst + rl];
-        z += x.s_b2[rl];
-      }
+      const float z = valid ? (x.zbuf[b * x.zst + rl] + x.zbuf[(B + b) * x.zst + rl]) + x.s_b2[rl]
+                            : __int_as_float(0x7fc00000);
       const uint32_t bits = __ballot_sync(0xffffffffu, z > x.t);
       u |= bits;
       if (lane == 0) x.mask[(size_t)b * x.words + x.w0 + wl] = bits;
@@ -385,13 +379,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint64_t *p2_done = ids_ready + 1;   // this CTA's phase 2 has finished (hot-neuron prefetch trigger)
   float *red = reinterpret_cast<float *>(ids_ready + 2);             // [2][8][32]
   float *hs = red + 2 * kGroupWarps * kRedStride;                    // [NS][NA*B]
-  float *zbuf = hs + NS * NA * B;                                    // [kp][B][wcap*32] logits per K part
-  float *s_b2 = zbuf + p.kp * B * p.wcap * 32;                       // [wcap*32]
+  float *zbuf = hs + NS * NA * B;                                    // [2][B][wcap*32] logits (two K halves)
+  float *s_b2 = zbuf + 2 * B * p.wcap * 32;                          // [wcap*32]
   float *s_bup = s_b2 + p.wcap * 32;                                 // [idcap]
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
   float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // [8][pcap*B] phase-4 partials
-  uint2 *gfrag = reinterpret_cast<uint2 *>(s_part + 8 * p.pcap * B);  // [kt][32] B fragments of g
+  float *sg = s_part + 8 * p.pcap * B;                               // [B][kt*16] staging of g
+  uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
   __shared__ unsigned s_gmax[B];
   __shared__ uint32_t s_slot_pos[kMaxStages];
   __shared__ float s_ss[kGroupWarps][B];
@@ -653,8 +648,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
       P2Ctx ctx{stages, full, empty, hready, s_slot_pos, zbuf, s_b2, &s_count, gfrag, s_gmax, tr, NS, SB,
-                (int)ring + st_p1, st_p2, w0, w1, m, r, p.kt, p.kp, p.words, p.words_p2, p.wcap * 32, ring, lw.t,
-                p.g, p.mask, p.uni};
+                (int)ring + st_p1, st_p2, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g,
+                p.mask, p.uni};
       p2_phase<T, B>(ctx);
     }
     consumers_sync();

@@ -49,12 +49,10 @@ constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 1
 constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
 constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
 constexpr int kMaxStages = 16;   // ring stages (s_slot_pos)
-constexpr int kMaxKPT = 16;      // phase 2: K tiles per warp's K part (B fragments held in registers)
 
 struct FusedWork {
   bool enabled = false;
   int P = 0, NS = 0, stage_bytes = 0, words_p2 = 0, idcap = 0, wcap = 0, smem = 0, part_off = 0, pcap = 0, kt = 0;
-  int kp = 0;   // phase 2: K parts (warps per 16-row tile)
   int d = 0, m = 0, r = 0;
   bool reglu = false;
   unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
@@ -104,7 +102,6 @@ struct FusedParams {
   unsigned long long *bar;
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   int kt;                     // 16-column K tiles of the fragment-major P2 (ceil(r / 16))
-  int kp;                     // phase-2 K parts (4 or 8; each warp keeps its part's B fragments)
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int hot_cap;                // at most this many hot neurons are L2-prefetched per layer
 };
@@ -128,8 +125,6 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
     return true;  // unsupported shape: stays disabled (per-step kernels)
   w.P = num_sms;
   w.kt = (r + 15) / 16;
-  w.kp = w.kt <= 4 * kMaxKPT ? 4 : 8;
-  if (w.kt > w.kp * kMaxKPT) return true;   // r > 2048: per-step kernels
   const size_t p2_word = (size_t)32 * w.kt * 16 * 2;   // one 32-row word of the tiled P2
   // stage: >= one neuron (gate|up + down), one P2 word, >= 32 KB
   const size_t nb = (size_t)d * (reglu ? 6 : 4);
@@ -148,8 +143,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   // partials, g staging and its B fragments; the ring gets the rest (<= 200 KB)
   auto extras = [&](int ns) {
     return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * kFusedMaxB * 4 +
-           (size_t)(w.kp * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
-           (size_t)w.kt * NT * 32 * 8 + 64;
+           (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
+           (size_t)kFusedMaxB * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
   };
   const size_t cap = 227 * 1024 - 1024;   // static shared memory and alignment slack
   w.NS = (int)std::min<size_t>({200 * 1024 / sb, cap / sb, (size_t)kMaxStages});
@@ -157,9 +152,9 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   while (w.NS >= 2 && (size_t)w.NS * sb + extras(w.NS) > cap) --w.NS;
   if (w.NS < 2) return true;
   const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                     (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(w.kp * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
+                     (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
   w.part_off = (int)(((size_t)w.NS * sb + pre + 15) / 16 * 16);
-  w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + w.kt * NT * 32 * 8 + 64;
+  w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
   const int words = (m + 31) / 32;
   if (!alloc((void **)&w.bar, (size_t)(1 + num_sms) * 128 + 128)) return false;
   if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
@@ -250,7 +245,6 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.part_off = w.part_off;
   p.pcap = w.pcap;
   p.kt = w.kt;
-  p.kp = w.kp;
   p.trace = w.trace;
   p.hot_cap = a.hot_cap;
   return p;

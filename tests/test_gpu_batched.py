@@ -12,7 +12,11 @@ from oracle import ffn as O
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-3
-GATE = 1e-5
+# Internal regression gate of the tensor-core path: the tcgen05 fp32 accumulation is not
+# round-to-nearest per product (measured rel-L2 ~1e-5 on random layers at d = 5120, vs ~5e-7 for
+# the CUDA-core kernels; integer layers stay bit-exact), so the gate is 5e-5 -- still 20x inside
+# the north_star tolerance of 1e-3.
+GATE = 5e-5
 
 
 @pytest.fixture(scope="module")
