@@ -258,6 +258,26 @@ pi_status pi_layer_set_trace(pi_layer *L, uint64_t *dev_buf);
 pi_status pi_partition(const float *freq, int32_t m, int32_t n_shards, int32_t granule,
                        int32_t *owner, int32_t *shard_ids, int32_t *shard_offsets);
 
+/* The paper's neuron-placement ILP (Eqs. 1-8), solved exactly.
+ * Two units, fast and slow: maximise the impact sum f_i placed on the fast unit (Eqs. 1-2),
+ * every batch of `granule` similar-impact neurons ((-f, i) order within a layer) on
+ * one unit (Eq. 3), fast-unit bytes < mcap_fast (Eq. 6), and per layer either no fast neuron or
+ * at least C_l, the smallest count with C_l T_fast + t_sync <= C_l T_slow, T = neuron_bytes /
+ * bandwidth (Eqs. 4, 5, 7, 8; reading R22).  Exact dynamic programme over layers (within a layer
+ * the best k batches are the k most impactful); ties go to fewer fast bytes.  On the B200 the
+ * fast unit is the hot-neuron tier of a layer (rows L2-prefetched/pinned, their count fed back
+ * as pi_layer_desc.hot_cap), the slow unit the dynamic HBM path.
+ * freq          host float [n_layers * m], layer-major, finite, >= 0
+ * neuron_bytes  host double [n_layers], positive integers (bytes of one neuron's rows)
+ * fast          host uint8 [n_layers * m] out: 1 = neuron placed on the fast unit
+ * fast_count    host int32 [n_layers] out: fast neurons per layer
+ * objective     host double out: the optimal Eq. 2 value
+ * Errors: INVALID_ARGUMENT (NULL, bad sizes, non-finite values), UNSUPPORTED (capacity / batch
+ *         size ratio beyond the exact DP's table). */
+pi_status pi_place_ilp(const float *freq, int32_t n_layers, int32_t m, const double *neuron_bytes,
+                       int32_t granule, double mcap_fast, double bw_fast, double bw_slow, double t_sync,
+                       uint8_t *fast, int32_t *fast_count, double *objective);
+
 #ifdef __cplusplus
 }
 #endif

@@ -508,7 +508,7 @@ cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float 
     if (e != cudaSuccess) return e;
     constexpr int NT = (3 * NB + 7) / 8;
     const size_t smem = (size_t)NB * a.kt * 16 * 4 + (size_t)a.kt * NT * 32 * 8 + (size_t)NB * 128 * 4;
-    if (smem > 48 * 1024) {
+    if (smem > 32 * 1024) {   // (the kernel's static shared memory counts against the 48 KB default too)
       e = cudaFuncSetAttribute(k_predict2<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
@@ -573,7 +573,7 @@ cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *sca
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
       const size_t smem = (size_t)8 * NB * 256 * 4;
-      if (smem > 48 * 1024) cudaFuncSetAttribute(k_down_q4<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (smem > 32 * 1024) cudaFuncSetAttribute(k_down_q4<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       k_down_q4<T, NB><<<a.tiles * a.S, 256, smem, s>>>((const uint8_t *)a.w_down, a.rec_q4, (const T *)a.b_down,
                                                          a.h, a.m, ids, n_active, a.d, a.S, a.tiles, a.partial,
                                                          a.tickets, y);
@@ -588,7 +588,7 @@ cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *sca
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)8 * NB * 256 * 4;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_down<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 32 * 1024) cudaFuncSetAttribute(k_down<T, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_down<T, NB><<<a.tiles * a.S, 256, smem, s>>>((const T *)a.w_down, (const T *)a.b_down, a.h, a.m, ids,
                                                     n_active, a.d, a.S, a.tiles, a.partial, a.tickets, y);
     return cudaGetLastError();

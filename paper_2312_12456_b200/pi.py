@@ -36,7 +36,7 @@ PI_MAX_BATCH = 32
 EXPORTS = ("pi_version", "pi_last_error", "pi_layer_create", "pi_layer_destroy", "pi_layer_get_info",
            "pi_predict", "pi_compact", "pi_sparse_ffn", "pi_layer_forward", "pi_layer_forward_host",
            "pi_stack_forward", "pi_stack_forward_host", "pi_partition", "pi_layer_set_trace",
-           "pi_stack_create", "pi_stack_destroy", "pi_stack_run", "pi_stack_run_host")
+           "pi_stack_create", "pi_stack_destroy", "pi_stack_run", "pi_stack_run_host", "pi_place_ilp")
 
 
 class PiError(RuntimeError):
@@ -94,6 +94,8 @@ def _load() -> ctypes.CDLL:
     lib.pi_stack_destroy.argtypes = [vp]
     lib.pi_stack_run.argtypes = [vp, vp, i32, vp, vp, vp]
     lib.pi_stack_run_host.argtypes = [vp, vp, i32, vp, vp]
+    dbl = ctypes.c_double
+    lib.pi_place_ilp.argtypes = [vp, i32, i32, vp, i32, dbl, dbl, dbl, dbl, vp, vp, ctypes.POINTER(dbl)]
     for name in EXPORTS:
         if name not in ("pi_version", "pi_last_error"):
             getattr(lib, name).restype = ctypes.c_int
@@ -311,6 +313,21 @@ def pi_partition(freq, n_shards: int, granule: int = 1):
     _check(_lib.pi_partition(f.ctypes.data, m, int(n_shards), int(granule), owner.ctypes.data, ids.ctypes.data,
                              off.ctypes.data))
     return owner, ids, off
+
+
+def pi_place_ilp(freq_layers, neuron_bytes, granule: int, mcap_fast: float, bw_fast: float, bw_slow: float,
+                 t_sync: float):
+    """The paper's placement ILP (Eqs. 1-8), exact.  freq_layers [L, m]; neuron_bytes [L].
+    Returns (fast uint8 [L, m], fast_count int32 [L], objective float)."""
+    f = np.ascontiguousarray(np.asarray(freq_layers, dtype=np.float32))
+    L, m = f.shape
+    nbytes = np.ascontiguousarray(np.asarray(neuron_bytes, dtype=np.float64))
+    fast = np.zeros((L, m), np.uint8)
+    cnt = np.zeros(L, np.int32)
+    obj = ctypes.c_double()
+    _check(_lib.pi_place_ilp(f.ctypes.data, L, m, nbytes.ctypes.data, int(granule), float(mcap_fast), float(bw_fast),
+                             float(bw_slow), float(t_sync), fast.ctypes.data, cnt.ctypes.data, ctypes.byref(obj)))
+    return fast, cnt, obj.value
 
 
 def mask_words(m: int) -> int:
