@@ -62,6 +62,11 @@ def parse():
     ap.add_argument("--rank", dest="pred_rank", type=int, default=None, help="predictor rank r override")
     ap.add_argument("--no-phases", action="store_true", help="skip the traced per-phase breakdown pass")
     ap.add_argument("--dry-run", action="store_true", help="CPU/gloo plumbing check, no kernels (numbers meaningless)")
+    ap.add_argument("--q4", action="store_true", help="INT4 weight-only FFN rows (PI_FFN_Q4, row f3)")
+    ap.add_argument("--placement", default="fixed", choices=["fixed", "ilp"],
+                    help="per-layer hot-neuron counts: fixed --hot-cap, or the paper's ILP (pi_place_ilp, row f4) "
+                         "under --l2-budget-mb")
+    ap.add_argument("--l2-budget-mb", type=float, default=60.0, help="fast-tier (L2) budget for --placement ilp")
     return ap.parse_args()
 
 
@@ -392,6 +397,21 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
 
+    # ---- per-layer hot-neuron counts from the paper's placement ILP (row f4) ----
+    ilp_caps, ilp_info = None, None
+    if args.placement == "ilp" and args.hot_freq > 0:
+        from paper_2312_12456_b200 import pi as _pi
+        prof = np.stack([gen.activity_profile(cfg.m, args.mean_act, seed=args.seed, layer=l) for l in range(n_layers)])
+        nbytes = [2 * (3 if cfg.act == "reglu" else 2) * cfg.d] * n_layers
+        peak_gbs = hbm_peak()[0]
+        # fast unit: L2-resident rows (~3x HBM bandwidth), slow: HBM; T_sync: one extra prefetch round
+        fast, cnt, obj = _pi.pi_place_ilp(prof, nbytes, 64, args.l2_budget_mb * 1e6, 3 * peak_gbs * 1e9,
+                                          peak_gbs * 1e9, 0.5e-6)
+        ilp_caps = [int(c) if c > 0 else 1 for c in cnt]
+        ilp_info = {"l2_budget_mb": args.l2_budget_mb, "hot_neurons_per_layer": [int(c) for c in cnt],
+                    "objective_expected_active_on_fast": round(obj, 2)}
+        args.hot_freq = 1e-9   # every neuron is eligible; the ILP count caps each layer
+
     # ---- build the workload (weights random-init with the config's architecture) ----
     single = n_layers == 1
     copies = args.copies if single else 1
@@ -399,7 +419,8 @@ def main():
     for c in range(copies):
         st, _ = build_stack(cfg, n_layers=n_layers, rank=rank, world=world, seed=args.seed + 1000 * c,
                             device=dev, max_batch=B, group=group, mean_act=args.mean_act, dims=layer_dims(args),
-                            hot_freq=args.hot_freq if args.hot_freq > 0 else None, hot_cap=args.hot_cap)
+                            hot_freq=args.hot_freq if args.hot_freq > 0 else None, hot_cap=args.hot_cap, q4=args.q4,
+                            hot_caps=ilp_caps)
         stacks.append(st)
     d = cfg.d
     T = args.warmup + args.steps
@@ -553,13 +574,16 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "int4" if args.q4 else cfg.dtype,
+               "data": "synthetic",
                "config": workload_config(cfg, B, n_layers, world, {
                    "realised_activity": round(realised, 4),
                    "l2": ("weights rotated over %d layer copies (> L2)" % copies) if single else
                          "inputs larger than L2 (every step streams %d layers; %.1f GB of FFN weights)" % (
                              n_layers, sum(L.info.weight_bytes for L in stacks[0].layers) / 1e9),
-                   "algorithmic_MB_per_step": round(float(bytes_step.sum(axis=1).mean()) / 1e6, 2)}, args=args),
+                   "algorithmic_MB_per_step": round(float(bytes_step.sum(axis=1).mean()) / 1e6, 2),
+                   "ffn_weights": "INT4 neuron rows (groups of 32, fp16 scales)" if args.q4 else cfg.dtype,
+                   "placement": ilp_info or "fixed"}, args=args),
                "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
                               "p99": float(np.percentile(per_step, 99))},
                "roofline": roofline, "phases_us": phases, "cpu_baseline": cpu, "e2e": e2e,

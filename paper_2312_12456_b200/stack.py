@@ -35,7 +35,8 @@ class LayerMeta:
     b_down: bool          # this shard owns b_down
     p_b1: bool
     p_b2: bool
-    e: int = 2            # bytes per weight element
+    e: int = 2            # bytes per weight element (predictor, biases; 16-bit FFN rows)
+    ffn_row_bytes: int = 0  # bytes of one neuron's row per FFN matrix (0: e * d; INT4: codes + scales)
 
 
 class Stack:
@@ -119,7 +120,7 @@ def shard_ids(p: np.ndarray, world: int, rank: int, granule: int = 64) -> Option
 def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, world: int = 1, seed: int = 0,
                 device="cuda", max_batch: int = 1, mean_act: float = 0.10, group=None,
                 keep_weights: bool = False, dims: Optional[dict] = None, hot_freq: Optional[float] = None,
-                hot_cap: int = 0):
+                hot_cap: int = 0, q4: bool = False, hot_caps: Optional[List[int]] = None):
     """Generate the config's layers (random init, seeded) and create this rank's handles.
 
     Returns (Stack, weights-or-None).  With keep_weights the generator tensors stay alive
@@ -135,12 +136,16 @@ def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, 
         own = rank == 0
         # the planted activity profile plays the paper's profiler frequencies f_i (Eq. 1)
         freq = None if hot_freq is None else w.p
+        qw = gen.make_q4(w) if q4 else None
         layers.append(pi.Layer(w, neuron_ids=nid, max_batch=max_batch, flags=flags, layer_id=l, own_b_down=own,
                                neuron_freq=freq, hot_freq=hot_freq if hot_freq is not None else 2.0,
-                               hot_cap=hot_cap))
+                               hot_cap=hot_caps[l] if hot_caps is not None else hot_cap, q4=qw))
+        del qw
         m_local = w.m if nid is None else len(nid)
+        rowb = ((w.d // 2 + w.d // 16 + 15) // 16) * 16 if q4 else 2 * w.d
         metas.append(LayerMeta(w.d, m_local, w.r, w.act == "reglu", w.b_up is not None,
-                               own and w.b_down is not None, w.p_b1 is not None, w.p_b2 is not None))
+                               own and w.b_down is not None, w.p_b1 is not None, w.p_b2 is not None,
+                               ffn_row_bytes=rowb))
         if keep_weights:
             kept.append((w, nid))
         else:
@@ -155,8 +160,9 @@ def algorithmic_bytes(meta: LayerMeta, n_union: int, B: int) -> int:
     realised union count.  Split-K partials, re-reads and over-fetch are NOT algorithmic."""
     e, d, r, m = meta.e, meta.d, meta.r, meta.m_local
     c = 3 if meta.reglu else 2
+    row = meta.ffn_row_bytes or e * d
     w = e * (r * d + r * m + (r if meta.p_b1 else 0) + (m if meta.p_b2 else 0))
-    w += e * c * n_union * d + (e * n_union if meta.b_up else 0) + (e * d if meta.b_down else 0)
+    w += c * n_union * row + (e * n_union if meta.b_up else 0) + (e * d if meta.b_down else 0)
     words = (m + 31) // 32
     io = 4 * B * d + 4 * B * d + 4 * B * words + 2 * 4 * n_union + 4 * B * r
     return int(w + io)
