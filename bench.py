@@ -58,6 +58,10 @@ def parse():
                          "neurons per layer whose profiled activation frequency is >= this, while the layer "
                          "synchronises after phase 2 (<= 0 disables; c4: 2.22 vs 2.30 ms/step)")
     ap.add_argument("--hot-cap", type=int, default=512, help="hot neurons prefetched per layer (pi_layer_desc.hot_cap)")
+    ap.add_argument("--spec-freq", type=float, default=0.99,
+                    help="speculative hot prefix (pi_layer_desc.spec_freq): neurons with profiled frequency >= this "
+                         "are computed while the grid synchronises after the predictor (<= 0 disables)")
+    ap.add_argument("--spec-cap", type=int, default=1 << 30, help="speculative neurons per layer (pi_layer_desc.spec_cap)")
     ap.add_argument("--mean-act", type=float, default=0.10, help="mean activity of the planted profile (5-20%%)")
     ap.add_argument("--rank", dest="pred_rank", type=int, default=None, help="predictor rank r override")
     ap.add_argument("--no-phases", action="store_true", help="skip the traced per-phase breakdown pass")
@@ -291,7 +295,10 @@ def workload_config(cfg, B, n_layers, N, extra=None, args=None):
          "mask_mode": "P (predictor-generated, planted b2)",
          "parallelism": "single GPU" if N == 1 else f"neuron-sharded x{N} (pi_partition) + NCCL all-reduce",
          "hot_neurons": ("L2 prefetch of <= %d neurons/layer with profiled frequency >= %g" %
-                         (args.hot_cap, hot_freq)) if hot_freq > 0 else "off"}
+                         (args.hot_cap, hot_freq)) if hot_freq > 0 else "off",
+         "speculative_prefix": ("neurons with profiled frequency >= %g computed while the grid synchronises "
+                                "after the predictor, corrected for tokens whose bit is 0" % args.spec_freq)
+         if args is not None and args.spec_freq > 0 else "off"}
     if extra:
         c.update(extra)
     return c
@@ -420,7 +427,7 @@ def main():
         st, _ = build_stack(cfg, n_layers=n_layers, rank=rank, world=world, seed=args.seed + 1000 * c,
                             device=dev, max_batch=B, group=group, mean_act=args.mean_act, dims=layer_dims(args),
                             hot_freq=args.hot_freq if args.hot_freq > 0 else None, hot_cap=args.hot_cap, q4=args.q4,
-                            hot_caps=ilp_caps)
+                            hot_caps=ilp_caps, spec_freq=args.spec_freq, spec_cap=args.spec_cap)
         stacks.append(st)
     d = cfg.d
     T = args.warmup + args.steps

@@ -118,6 +118,16 @@ typedef struct {
   const float *neuron_freq;
   float hot_freq;
   int32_t hot_cap;
+  /* Speculative hot prefix (Insight-1: ~3% of neurons fire for ~every token): neurons
+   * of this shard with f_i >= spec_freq (hottest first, at most spec_cap; spec_freq <= 0 or
+   * spec_cap <= 0 disables) are, in a stack launch (pi_stack_run), computed BEFORE the layer's
+   * mask is known -- their rows stream and their up/down products accumulate while the grid
+   * synchronises and compacts after the predictor -- and corrected afterwards (their down
+   * contribution subtracted) for every token whose predicted bit is 0.  Results equal the
+   * non-speculative path up to fp32 summation order (bit for bit on integer-exact layers).
+   * Speculative neurons are not L2-prefetched again by the hot-neuron prefetch. */
+  float spec_freq;
+  int32_t spec_cap;
   pi_ffn_format ffn_format;  /* PI_FFN_16 (default, 0) or PI_FFN_Q4                         */
   const void *w_up_scale;    /* PI_FFN_Q4: dev fp16 [m_total, d/32]; else NULL               */
   const void *w_gate_scale;  /* PI_FFN_Q4 and REGLU: dev fp16 [m_total, d/32]; else NULL     */
@@ -133,6 +143,7 @@ typedef struct {
   int64_t workspace_bytes;  /* library-owned workspace bytes                        */
   int32_t launches_per_forward; /* kernel launches one pi_layer_forward call makes   */
   int32_t ffn_format;           /* pi_ffn_format                                      */
+  int32_t n_spec;               /* speculative hot-prefix neurons of this handle      */
 } pi_layer_info;
 
 /* Library version string, e.g. "libpi 0.1.0 sm_100a". */

@@ -185,7 +185,8 @@ struct P2Ctx {
   uint64_t *full, *empty, *hready;
   volatile uint32_t *slot_pos;   // [NS] ring position the producer last acquired each slot for
   float *zbuf, *s_b2;
-  int *s_count;
+  int *s_count, *s_count_full;   // this CTA's union counts: without / with the speculative neurons
+  const uint32_t *spec_words;    // speculative-neuron bitmap (NULL: none); cleared from the union words
   uint2 *gfrag;                  // [kt][NT][32] shared B fragments
   unsigned *gmax;                // [B] shared max |g| bits (fp16 scaling), zeroed at layer start
   unsigned long long *trace;
@@ -332,8 +333,9 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
   if (dt && warp == 0) dt[3] = globaltimer();
-  // ballots: one warp per mask word -> per-token words, union word, popcount
-  int my_count = 0;
+  // ballots: one warp per mask word -> per-token words, union word (without the speculative
+  // neurons, which are computed before the compaction), popcounts
+  int my_count = 0, my_full = 0;
   for (int wl = warp; wl < x.w1 - x.w0; wl += kConsumerWarps) {
     const int rl = wl * 32 + lane;
     const bool valid = (x.w0 * 32 + rl) < x.m;
@@ -347,11 +349,14 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       if (lane == 0) x.mask[(size_t)b * x.words + x.w0 + wl] = bits;
     }
     if (lane == 0) {
-      x.uni[x.w0 + wl] = u;
-      my_count += __popc(u);
+      const uint32_t uc = x.spec_words ? (u & ~x.spec_words[x.w0 + wl]) : u;
+      x.uni[x.w0 + wl] = uc;
+      my_count += __popc(uc);
+      my_full += __popc(u);
     }
   }
   if (lane == 0 && my_count) atomicAdd(x.s_count, my_count);
+  if (lane == 0 && my_full) atomicAdd(x.s_count_full, my_full);
   if (x.trace && tid == 0) x.trace[3] = globaltimer();
 }
 
@@ -389,6 +394,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
   __shared__ unsigned s_gmax[B];
   __shared__ uint32_t s_slot_pos[kMaxStages];
+  // speculative hot prefix (this CTA's share) and its corrections
+  __shared__ int32_t s_spec_ids[kMaxSpecPerCta];
+  __shared__ float s_bspec[kMaxSpecPerCta];
+  __shared__ float s_hspec[kMaxSpecPerCta][B];
+  __shared__ int32_t s_corr_ids[kMaxCorrPerCta];
+  __shared__ float s_corr_h[kMaxCorrPerCta][B];
+  __shared__ int s_ncorr, s_count_full;
+  __shared__ __align__(8) uint64_t s_b2_arrive, s_b2_done;   // split-phase grid barrier 2
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
@@ -418,6 +431,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     mbar_init(ids_ready, 1);
     mbar_init(p2_done, 1);
     for (int s = 0; s < kMaxStages; ++s) s_slot_pos[s] = 0xffffffffu;
+    mbar_init(&s_b2_arrive, 1);
+    mbar_init(&s_b2_done, 1);
   }
   for (int i = tid; i < p.kt * 32; i += blockDim.x) gfrag[i] = make_uint2(0u, 0u);
   if (tid == 0) {
@@ -430,6 +445,32 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   // rows while the consumers finish the current layer (bounded by the ring)
   // =====================================================================================
   if (warp == kConsumerWarps) {
+    if (lane == 1) {
+      // barrier agent: grid barrier 2 of layers with a speculative prefix is split -- the
+      // consumers signal their arrival and go on computing the speculative neurons while this
+      // lane does the global arrive and poll, then releases them through s_b2_done
+      int ns = 0;
+      for (int l = 0; l < L; ++l) {
+        if (!(p.spec && layer(l).n_spec > 0)) continue;
+        mbar_wait(&s_b2_arrive, ns & 1);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        unsigned long long old;
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.bar) : "memory");
+        const unsigned long long target = (old / (unsigned long long)P + 1ull) * (unsigned long long)P;
+        const unsigned long long t0 = globaltimer();
+        while (true) {
+          unsigned long long cur;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(p.bar) : "memory");
+          if (cur >= target) break;
+          __nanosleep(32);
+          if (globaltimer() - t0 > 4000000000ull) __trap();
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        mbar_arrive(&s_b2_done);
+        ++ns;
+      }
+      return;
+    }
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
     uint32_t it = 0, trace_it0 = 0xffffffffu;
@@ -502,6 +543,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
       }
       prefetch_tail(NS);
+      // speculative hot prefix: static ids, no dependency on this layer's mask -- streamed right
+      // behind the P2 stages, consumed while the grid synchronises and compacts
+      const int n_spec_c = (p.spec && lw.n_spec > c) ? (lw.n_spec - 1 - c) / P + 1 : 0;
+      for (int k0 = 0; k0 < n_spec_c; k0 += G, ++it) {
+        const int kn = min(G, n_spec_c - k0);
+        uint8_t *dst = acquire((uint32_t)(kn * nb));
+        const int s = it % NS;
+        for (int k = 0; k < kn; ++k) {
+          const int i = lw.spec_ids[c + (k0 + k) * P];
+          bulk_g2s(dst + (size_t)k * nb, lw.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
+          bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+        }
+      }
       if (lw.n_hot) {
         // hot neurons (activation frequency >= hot_freq) are almost surely active: once this
         // CTA's phase 2 is done (its P2 stages are in, HBM idles through barrier 2 and the
@@ -528,6 +582,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
         }
       }
+      // corrections of speculative neurons whose bit is 0 for some token: their down rows again
+      const int n_corr = s_ncorr;
+      for (int k0 = 0; k0 < n_corr; k0 += G, ++it) {
+        const int kn = min(G, n_corr - k0);
+        uint8_t *dst = acquire((uint32_t)(kn * row_dn));
+        const int s = it % NS;
+        for (int k = 0; k < kn; ++k) {
+          const int i = s_corr_ids[k0 + k];
+          bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+        }
+      }
     }
     // drain: do not retire before the consumers released every stage
     for (uint32_t j = (it > (uint32_t)NS ? it - NS : 0); j < it; ++j) mbar_wait(&empty[j % NS], (j / NS) & 1);
@@ -542,6 +607,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   const int gw = gt >> 5;                      // warp index inside its group
   auto stage_ptr = [&](uint32_t it) { return stages + (size_t)(it % NS) * SB; };
   uint32_t ring = 0;                           // ring position of this layer's first stage
+  int n_spec_layers = 0;                       // layers with a speculative prefix so far (s_b2_* parity)
 
   for (int l = 0; l < L; ++l) {
     const LayerW lw = layer(l);
@@ -553,8 +619,20 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       mbar_wait(&full[it % NS], (it / NS) & 1);
       if (tr && tid == 0 && it - ring0 < 56) tr[16 + it - ring0] = globaltimer();
     };
-    if (tid == 0) s_count = 0;
+    if (tid == 0) {
+      s_count = 0;
+      s_count_full = 0;
+      s_ncorr = 0;
+    }
     if (tid < B) s_gmax[tid] = 0u;
+    // this CTA's share of the speculative hot prefix: neurons c, c + P, ... of the layer's list
+    const bool spec_on = p.spec && lw.n_spec > 0;
+    const int n_spec_c = spec_on && lw.n_spec > c ? (lw.n_spec - 1 - c) / P + 1 : 0;
+    for (int k = tid; k < n_spec_c; k += kConsumers) {
+      const int i = lw.spec_ids[c + k * P];
+      s_spec_ids[k] = i;
+      s_bspec[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
+    }
     if (tr && tid == 0) tr[0] = globaltimer();
 
     float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
@@ -647,34 +725,145 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 
     // ---------------- phase 2 (all 16 consumer warps): z = P2 g + b2, bits, union, counts ----------------
     {
-      P2Ctx ctx{stages, full, empty, hready, s_slot_pos, zbuf, s_b2, &s_count, gfrag, s_gmax, tr, NS, SB,
-                (int)ring + st_p1, st_p2, w0, w1, m, r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g,
-                p.mask, p.uni};
+      P2Ctx ctx{stages, full, empty, hready, s_slot_pos, zbuf, s_b2, &s_count, &s_count_full,
+                spec_on ? lw.spec_words : nullptr, gfrag, s_gmax, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
+                r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
       p2_phase<T, B>(ctx);
     }
     consumers_sync();
     if (tid == 0) {
       p.counts[c] = s_count;
+      p.counts_full[c] = s_count_full;
       mbar_arrive(p2_done);
     }
-    grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
+
+    // ---------------- FFN stage processing (shared by the speculative, cold and correction stages) ----------------
+    //   up group  : up (and gate) dots of the stage's kn neurons, h = act(.) -> hs (+ hsave)
+    //   down group: y_part += h * down row (register-resident partial y)
+    float yr[CH][8][B];
+#pragma unroll
+    for (int q = 0; q < CH; ++q)
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+#pragma unroll
+        for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
+    // bup_s[g] = b_up of the stage's g-th neuron; bits_s[g] = its per-token bits (NULL: all set);
+    // hsave[g][b] receives h (speculative stages)
+    auto up_stage = [&](uint32_t it, int kn, const float *bup_s, const uint8_t *bits_s, float (*hsave)[B]) {
+      constexpr int NV = NA * B * (REGLU ? 2 : 1);
+      wait_full(it);
+      const uint8_t *buf = stage_ptr(it);
+      float acc[NV];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int g = 0; g < NA; ++g) {
+        const size_t go = (size_t)g * nb;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int ch = gt + q * kGroup;
+          const bool ok = g < kn && ch < chunks;
+          float wu[8];
+          if (REGLU) {
+            float wg[8];
+            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
+            WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+          } else {
+            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
+          }
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+              acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+            }
+        }
+      }
+      float *rb = red + (it & 1) * kGroupWarps * kRedStride;
+      up_partials<NV>(acc, rb);
+      if (warp == 0) {
+        if (lane < kn * B) {
+          const int g = lane / B, b = lane % B;
+          const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + bup_s[g];
+          const float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
+          hs[(it % NS) * (NA * B) + lane] = (!bits_s || ((bits_s[g] >> b) & 1)) ? hv : 0.f;
+          if (hsave) hsave[g][b] = hv;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&hready[it % NS]);
+      }
+    };
+    auto down_stage = [&](uint32_t it, int kn) {
+      wait_full(it);
+      mbar_wait(&hready[it % NS], (it / NS) & 1);
+      const uint8_t *buf = stage_ptr(it);
+      const float *hh = hs + (it % NS) * (NA * B);
+#pragma unroll
+      for (int g = 0; g < NA; ++g) {
+        float h[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
+        const size_t go = (size_t)g * nb + row_up;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int ch = gt + q * kGroup;
+          float wf[8];
+          WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
+#pragma unroll
+          for (int b = 0; b < B; ++b)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
+    };
+
+    // ---------------- grid barrier 2; with a speculative prefix it is split around the speculative stages ----------------
+    const uint32_t it_spec = ring + st_p1 + st_p2;
+    const int n_spec_st = (n_spec_c + G - 1) / G;
+    if (spec_on) {
+      if (tid == 0) mbar_arrive(&s_b2_arrive);   // the agent lane arrives globally and polls
+      for (int f = 0; f < n_spec_st; ++f) {
+        const int kk = f * G, kn = min(G, n_spec_c - kk);
+        if (is_up) up_stage(it_spec + f, kn, s_bspec + kk, nullptr, &s_hspec[kk]);
+        else down_stage(it_spec + f, kn);
+      }
+      mbar_wait(&s_b2_done, n_spec_layers & 1);
+      ++n_spec_layers;
+      consumers_sync();
+    } else {
+      grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
+    }
     if (tr && tid == 0) tr[4] = globaltimer();
 
     // ---------------- phase 3: compaction of my share ----------------
-    // One L2 round trip: all consumer threads stage the P counts, the union words and (B > 1)
-    // the per-token words into the ring slot the first FFN stage will use -- free now: every
-    // predictor stage has been consumed and the producer waits for ids_ready before reusing it.
-    const uint32_t it_ffn = ring + st_p1 + st_p2;
+    // One L2 round trip: all consumer threads stage the P counts, the union words and the
+    // per-token words (B > 1, or for the speculative corrections) into the ring slot the first
+    // cold FFN stage will use -- free now: every earlier stage has been consumed and the producer
+    // waits for ids_ready before reusing it.
+    const bool stage_tok = B > 1 || spec_on;
+    const uint32_t it_ffn = it_spec + n_spec_st;
     uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
-    uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (B > 1)
-    int *c_cnt = reinterpret_cast<int *>(c_msk + (B > 1 ? B * p.words : 0));   // [P]
+    uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (stage_tok)
+    int *c_cnt = reinterpret_cast<int *>(c_msk + (stage_tok ? B * p.words : 0));   // [P]
+    int *c_cntf = c_cnt + P;                                              // [P] (spec_on)
     for (int i = tid; i < p.words; i += kConsumers) {
       c_uni[i] = __ldcg(p.uni + i);
-      if (B > 1)
+      if (stage_tok)
 #pragma unroll
         for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
     }
-    if (tid < P) c_cnt[tid] = __ldcg(p.counts + tid);
+    if (tid < P) {
+      c_cnt[tid] = __ldcg(p.counts + tid);
+      if (spec_on) c_cntf[tid] = __ldcg(p.counts_full + tid);
+    }
     consumers_sync();
     if (warp == 0) {
       // CTA-block b owns words [b W/P, (b+1) W/P)
@@ -744,18 +933,48 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           w += 32;
         }
       }
+      int nfull = n;
+      if (spec_on) {   // the layer's union count includes the speculative neurons
+        int fs = 0;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) fs += (lane * KPL + i < P) ? c_cntf[lane * KPL + i] : 0;
+        nfull = __reduce_add_sync(0xffffffffu, fs);
+      }
       if (lane == 0) {
-        s_n = n;
+        s_n = nfull;
         s_k0 = k0;
         s_k1 = k1;
       }
+    } else if (warp == 1) {
+      // corrections: my speculative neurons whose bit is 0 for some token (ascending k, fixed order)
+      int nc = 0;
+      for (int k0 = 0; k0 < n_spec_c; k0 += 32) {
+        const int kk = k0 + lane;
+        bool need = false;
+        uint32_t tb = 0;
+        if (kk < n_spec_c) {
+          const int i = s_spec_ids[kk];
+#pragma unroll
+          for (int b = 0; b < B; ++b) tb |= ((c_msk[b * p.words + (i >> 5)] >> (i & 31)) & 1u) << b;
+          need = tb != (1u << B) - 1u;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, need);
+        if (need) {
+          const int slot = nc + __popc(bal & ((1u << lane) - 1u));
+          s_corr_ids[slot] = s_spec_ids[kk];
+#pragma unroll
+          for (int b = 0; b < B; ++b) s_corr_h[slot][b] = ((tb >> b) & 1u) ? 0.f : -s_hspec[kk][b];
+        }
+        nc += __popc(bal);
+      }
+      if (lane == 0) s_ncorr = nc;
     }
     // generic-proxy writes to the scratch slot before the producer's TMA overwrites it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     consumers_sync();
     if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
     if (tr && tid == 0) tr[5] = globaltimer();
-    const int k0 = s_k0, n_mine = s_k1 - s_k0;
+    const int k0 = s_k0, n_mine = s_k1 - s_k0, n_corr = s_ncorr;
     for (int k = tid; k < n_mine; k += kConsumers) {
       const int i = s_ids[k];
       s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
@@ -764,96 +983,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
     consumers_sync();
 
-    // ---------------- phase 3: the sparse FFN ----------------
+    // ---------------- phase 3: the sparse FFN over the cold ids, then the corrections ----------------
     const int n_st = (n_mine + G - 1) / G;
-    if (is_up) {
-      constexpr int NV = NA * B * (REGLU ? 2 : 1);
-      for (int f = 0; f < n_st; ++f) {
-        const uint32_t it = it_ffn + f;
-        const int kk = f * G, kn = min(G, n_mine - kk);
+    for (int f = 0; f < n_st; ++f) {
+      const int kk = f * G, kn = min(G, n_mine - kk);
+      if (is_up) up_stage(it_ffn + f, kn, s_bup + kk, s_bits + kk, nullptr);
+      else down_stage(it_ffn + f, kn);
+    }
+    const uint32_t it_corr = it_ffn + n_st;
+    const int n_corr_st = (n_corr + G - 1) / G;
+    for (int f = 0; f < n_corr_st; ++f) {
+      const uint32_t it = it_corr + f;
+      const int kk = f * G, kn = min(G, n_corr - kk);
+      if (is_up) {
+        // h of a correction = minus the speculative h of each token whose bit is 0 (0 otherwise)
         wait_full(it);
-        const uint8_t *buf = stage_ptr(it);
-        float acc[NV];
-#pragma unroll
-        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
-#pragma unroll
-        for (int g = 0; g < NA; ++g) {
-          const size_t go = (size_t)g * nb;
-#pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int ch = gt + q * kGroup;
-            const bool ok = g < kn && ch < chunks;
-            float wu[8];
-            if (REGLU) {
-              float wg[8];
-              WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
-              WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
-#pragma unroll
-              for (int b = 0; b < B; ++b)
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
-            } else {
-              WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
-            }
-#pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-                acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
-              }
-          }
-        }
-        float *rb = red + (f & 1) * kGroupWarps * kRedStride;
-        up_partials<NV>(acc, rb);
         if (warp == 0) {
-          if (lane < kn * B) {
-            const int g = lane / B, b = lane % B;
-            const int slot = kk + g;
-            const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + s_bup[slot];
-            float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
-            hs[(it % NS) * (NA * B) + lane] = ((s_bits[slot] >> b) & 1) ? hv : 0.f;
-          }
+          if (lane < kn * B) hs[(it % NS) * (NA * B) + lane] = s_corr_h[kk + lane / B][lane % B];
           __syncwarp();
           if (lane == 0) mbar_arrive(&hready[it % NS]);
         }
+      } else {
+        down_stage(it, kn);
       }
-    } else {
-      float yr[CH][8][B];
-#pragma unroll
-      for (int q = 0; q < CH; ++q)
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-#pragma unroll
-          for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
-      for (int f = 0; f < n_st; ++f) {
-        const uint32_t it = it_ffn + f;
-        const int kn = min(G, n_mine - f * G);
-        wait_full(it);
-        mbar_wait(&hready[it % NS], (it / NS) & 1);
-        const uint8_t *buf = stage_ptr(it);
-        const float *hh = hs + (it % NS) * (NA * B);
-#pragma unroll
-        for (int g = 0; g < NA; ++g) {
-          float h[B];
-#pragma unroll
-          for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
-          const size_t go = (size_t)g * nb + row_up;
-#pragma unroll
-          for (int q = 0; q < CH; ++q) {
-            const int ch = gt + q * kGroup;
-            float wf[8];
-            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
-#pragma unroll
-            for (int b = 0; b < B; ++b)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
-      }
+    }
+    if (!is_up) {
       // partial y of this CTA -> global
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
@@ -868,7 +1022,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         }
       }
     }
-    ring = it_ffn + n_st;
+    ring = it_corr + n_corr_st;
 
     if (tr && tid == 0) tr[6] = globaltimer();
     grid_sync(p.bar, P, tr ? tr + 208 : nullptr);

@@ -49,6 +49,8 @@ constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 1
 constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
 constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
 constexpr int kMaxStages = 16;   // ring stages (s_slot_pos)
+constexpr int kMaxSpecPerCta = 32;   // speculative hot-prefix neurons per CTA (static shared tables)
+constexpr int kMaxCorrPerCta = 32;   // corrections per CTA and layer (more: the rest run unspeculated)
 
 struct FusedWork {
   bool enabled = false;
@@ -59,6 +61,7 @@ struct FusedWork {
   float *g = nullptr;                 // [maxB, r]
   float *ypart = nullptr;             // [P, maxB, d]
   int *counts = nullptr;              // [P]
+  int *counts_full = nullptr;         // [P]
   uint32_t *mask = nullptr;           // [maxB, words]
   uint32_t *uni = nullptr;            // [words]
   float *xbuf = nullptr;              // [maxB, d] inter-layer activations (stack launch)
@@ -84,6 +87,9 @@ struct LayerW {  // one layer's library-owned weights (device pointers)
   const int32_t *hot_ids;   // local ids of the hot neurons (L2-prefetched each step), or NULL
   int n_hot;
   float t;
+  const int32_t *spec_ids;      // speculative hot prefix (hottest first), or NULL
+  const uint32_t *spec_words;   // [words] bitmap of the speculative neurons
+  int n_spec;
 };
 
 struct FusedParams {
@@ -99,7 +105,9 @@ struct FusedParams {
   int32_t *ids_out, *n_out;   // n_out: [L] union counts
   float *g, *ypart;
   int *counts;
+  int *counts_full;           // [P] per-CTA union counts incl. the speculative neurons
   unsigned long long *bar;
+  int spec;                   // speculative hot prefix on (stack launches only)
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   int kt;                     // 16-column K tiles of the fragment-major P2 (ceil(r / 16))
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
@@ -131,7 +139,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, p2_word});
   sb = (sb + 127) / 128 * 128;
   // compaction stages the union words, the per-token words and the P counts in one ring slot
-  if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)num_sms * 4 > sb) return true;
+  if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)2 * num_sms * 4 > sb) return true;
   w.stage_bytes = (int)sb;
   w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / p2_word));
   w.idcap = (m + w.P - 1) / w.P + 2;
@@ -146,7 +154,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
            (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
            (size_t)kFusedMaxB * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
   };
-  const size_t cap = 227 * 1024 - 1024;   // static shared memory and alignment slack
+  const size_t cap = 227 * 1024 - 2560;   // static shared memory (speculative tables, barriers) and slack
   w.NS = (int)std::min<size_t>({200 * 1024 / sb, cap / sb, (size_t)kMaxStages});
   if ((size_t)w.kt * 12 * kFusedMaxB > (size_t)3 * kConsumers) return true;   // p2_phase: <= 3 entries per thread
   while (w.NS >= 2 && (size_t)w.NS * sb + extras(w.NS) > cap) --w.NS;
@@ -160,6 +168,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
   if (!alloc((void **)&w.ypart, (size_t)w.P * std::min(maxB, kFusedMaxB) * d * 4)) return false;
   if (!alloc((void **)&w.counts, (size_t)w.P * 4)) return false;
+  if (!alloc((void **)&w.counts_full, (size_t)w.P * 4)) return false;
   if (!alloc((void **)&w.mask, (size_t)maxB * words * 4)) return false;
   if (!alloc((void **)&w.uni, (size_t)words * 4)) return false;
   if (!alloc((void **)&w.xbuf, (size_t)std::min(maxB, kFusedMaxB) * d * 4)) return false;
@@ -236,6 +245,7 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.g = w.g;
   p.ypart = w.ypart;
   p.counts = w.counts;
+  p.counts_full = w.counts_full;
   p.bar = w.bar;
   p.NS = w.NS;
   p.stage_bytes = w.stage_bytes;
@@ -278,6 +288,7 @@ inline cudaError_t fused_launch_stack(FusedWork &w, const FusedArgs &a, const La
   p.L = L;
   p.mask = w.mask;
   p.ids_out = nullptr;
+  p.spec = 1;   // layers without a speculative table (n_spec == 0) run unspeculated
   return fused_launch_p<T>(w, p, a.reglu, a.B, s);
 }
 

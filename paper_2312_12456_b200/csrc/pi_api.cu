@@ -89,6 +89,9 @@ struct pi_layer {
   int S_tc = 0;
   int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons, hottest first
   int n_hot = 0, hot_cap = 0;
+  int32_t *spec_ids = nullptr;             // [n_spec] speculative hot prefix, hottest first
+  uint32_t *spec_words = nullptr;          // [words] bitmap of the speculative neurons
+  int n_spec = 0;
   FusedWork fw{};             // fused-kernel workspace
   int tiles = 0, S = 0;
   int64_t weight_bytes = 0, ws_bytes = 0;
@@ -294,14 +297,36 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   cudaStream_t s = (cudaStream_t)stream;
   L->hot_cap = D->hot_cap > 0 ? D->hot_cap : PI_DEFAULT_HOT_CAP;
   if (D->neuron_freq) {
+    auto freq_of = [&](int k) { return D->neuron_freq[D->neuron_ids ? D->neuron_ids[k] : k]; };
+    // speculative hot prefix: f >= spec_freq, hottest first (ties: ascending id), <= spec_cap
+    std::vector<int32_t> spec;
+    std::vector<uint8_t> is_spec(ml, 0);
+    if (D->spec_freq > 0.f && D->spec_cap > 0 && L->fw.enabled) {
+      for (int k = 0; k < ml; ++k)
+        if (std::isfinite(freq_of(k)) && freq_of(k) >= D->spec_freq) spec.push_back(k);
+      std::stable_sort(spec.begin(), spec.end(), [&](int a, int b) { return freq_of(a) > freq_of(b); });
+      const int cap = std::min(D->spec_cap, kMaxSpecPerCta * L->num_sms);
+      if ((int)spec.size() > cap) spec.resize(cap);
+      for (int k : spec) is_spec[k] = 1;
+    }
+    if (!spec.empty()) {
+      std::vector<uint32_t> words(L->words, 0u);
+      for (int k : spec) words[k >> 5] |= 1u << (k & 31);
+      st = dev_alloc(L, (void **)&L->spec_ids, spec.size() * 4, false);
+      if (st != PI_OK) return cleanup(st);
+      st = dev_alloc(L, (void **)&L->spec_words, (size_t)L->words * 4, false);
+      if (st != PI_OK) return cleanup(st);
+      if (cudaMemcpy(L->spec_ids, spec.data(), spec.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+          cudaMemcpy(L->spec_words, words.data(), words.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        return cleanup(fail(PI_ERR_CUDA, "layer %d: speculative table copy", lid));
+      L->n_spec = (int)spec.size();
+    }
+    // hot-neuron L2 prefetch list: f >= hot_freq, not speculative, hottest first
     std::vector<int32_t> hot;
     for (int k = 0; k < ml; ++k) {
-      const int gid = D->neuron_ids ? D->neuron_ids[k] : k;
-      const float f = D->neuron_freq[gid];
-      if (std::isfinite(f) && f >= D->hot_freq) hot.push_back(k);
+      const float f = freq_of(k);
+      if (!is_spec[k] && std::isfinite(f) && f >= D->hot_freq) hot.push_back(k);
     }
-    // hottest first (ties: ascending id), so the kernel's per-layer cap keeps the most frequent
-    auto freq_of = [&](int k) { return D->neuron_freq[D->neuron_ids ? D->neuron_ids[k] : k]; };
     std::stable_sort(hot.begin(), hot.end(), [&](int a, int b) { return freq_of(a) > freq_of(b); });
     if (!hot.empty()) {
       st = dev_alloc(L, (void **)&L->hot_ids, hot.size() * 4, false);
@@ -428,6 +453,9 @@ extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, 
     h[l].t = Ll->threshold;
     h[l].hot_ids = Ll->hot_ids;
     h[l].n_hot = std::min(Ll->n_hot, Ll->hot_cap);
+    h[l].spec_ids = Ll->spec_ids;
+    h[l].spec_words = Ll->spec_words;
+    h[l].n_spec = Ll->n_spec;
   }
   if (cudaMalloc(&S->lws, sizeof(LayerW) * n_layers) != cudaSuccess) {
     delete S;
@@ -520,6 +548,7 @@ extern "C" pi_status pi_layer_get_info(const pi_layer *L, pi_layer_info *info) {
   info->weight_bytes = L->weight_bytes;
   info->workspace_bytes = L->ws_bytes;
   info->ffn_format = L->ffn;
+  info->n_spec = L->n_spec;
   info->launches_per_forward =
       (!(L->flags & PI_FLAG_MULTI_KERNEL) && fused_supported(L->fw, 1)) ? 1
                                                                         : 5 + ((L->flags & PI_FLAG_INPUT_RMSNORM) ? 1 : 0);

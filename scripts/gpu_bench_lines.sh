@@ -14,7 +14,8 @@ try:
 except Exception as e:
     print('$n FAILED', e); print(open('gpurun_out/lines/$n.err').read()[-1500:])"
 }
-for cfgb in ${LINES:-"c3:1 c3:2 c3:4 c3:8 c3:16 c3:32 c4q4:1 c2:1 c1:1"}; do
+LINES=${LINES:-c3:1 c3:2 c3:4 c3:8 c3:16 c3:32 c4q4:1 c2:1 c1:1}
+for cfgb in $LINES; do
   c=${cfgb%%:*}; bb=${cfgb##*:}
   case $c in
     c4q4) run c4_q4_b$bb --config c4 --batch $bb --q4 --hot-freq 0 ;;

@@ -550,3 +550,74 @@ def test_full_size_c4_stack_bench_configuration(env):
         st.close()
         torch.cuda.empty_cache()
     assert torch.equal(outs[0], outs[1])
+
+
+# ---------------------------------------------------------------------------
+# speculative hot prefix (pi_layer_desc.spec_freq; stack launches)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("B", [1, 2])
+@pytest.mark.parametrize("act", ["relu", "reglu"])
+def test_speculative_prefix_integer_bitwise(env, B, act):
+    """Integer-exact layer through a one-layer stack launch with ~40% of the neurons speculative --
+    many of them predicted inactive, so the correction path runs -- equals the oracle bit for bit
+    (add-then-subtract is exact on integers)."""
+    gen, pi = env
+    d, m, r = (256, 1000, 64) if act == "relu" else (64, 250, 16)
+    w = gen.make_int_layer(d, m, r, act, seed=d + m + B + 3, dtype="bf16", device="cuda")
+    freq = np.random.default_rng(B).random(m).astype(np.float32)
+    L = pi.Layer(w, max_batch=2, neuron_freq=freq, spec_freq=0.6, hot_freq=2.0)
+    assert L.info.n_spec > 0
+    S = pi.StackHandle([L])
+    x = gen.int_tokens(B, d, act, seed=B + 7).cuda()
+    y = torch.empty(B, d, device="cuda")
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    S.run(x, y, n)
+    torch.cuda.synchronize()
+    xo = f(x).astype(np.float64)
+    om, z = O.predict(xo, f(w.p_w1), f(w.p_b1), f(w.p_w2), f(w.p_b2), 0.5)
+    ids = O.compact(om)
+    assert int(n.item()) == len(ids)                 # the union count includes the speculative neurons
+    spec = freq >= 0.6
+    assert (spec & ~om.any(axis=0)).sum() > 10       # corrections were exercised
+    yo = O.sparse_ffn(xo, ids, om, f(w.w_up), f(w.b_up), f(w.w_gate), f(w.w_down), f(w.b_down), act)
+    assert (y.cpu().numpy() == yo).all()
+    S.close()
+
+
+@pytest.mark.parametrize("name,dims,B", [("c4", (2048, 4096, 64), 1), ("c3", (1024, 2000, 64), 2),
+                                         ("c4", (8192, 32768, 512), 1)])
+def test_speculative_prefix_stack_matches(env, name, dims, B):
+    """Random layers (planted profile as neuron_freq, spec_freq 0.99 as in the bench): the stack with
+    the speculative prefix equals the stack without it up to fp32 summation order, and both equal
+    the layer chain's oracle check (per layer on the GPU's own input, R20)."""
+    gen, pi = env
+    from paper_2312_12456_b200.stack import build_stack
+    cfg = gen.CONFIGS[name]
+    dd = {"d": dims[0], "m": dims[1], "r": dims[2]}
+    x = gen.tokens(B, dims[0], seed=3, device="cuda")
+    outs = []
+    for spec in (0.0, 0.99):
+        st, kept = build_stack(cfg, n_layers=4, seed=2, device="cuda", max_batch=2, keep_weights=(spec > 0),
+                               dims=dd, hot_freq=0.9, spec_freq=spec)
+        if spec > 0:
+            assert st.layers[0].info.n_spec > 0
+        y = torch.empty(B, dims[0], device="cuda")
+        st.step(x, y)
+        torch.cuda.synchronize()
+        for _ in range(3):   # deterministic run to run
+            y2 = torch.empty_like(y)
+            st.step(x, y2)
+            torch.cuda.synchronize()
+            assert torch.equal(y2, y)
+        outs.append(y.cpu().numpy())
+        if spec > 0:
+            cur = x
+            for l, (w, _) in enumerate(kept):
+                yl, gm, ids, nl = run_forward(pi, st.layers[l], cur)   # single-layer launches: unspeculated
+                oracle_check(w, cur, yl, gm, ids, norm=cfg.rmsnorm)
+                cur = torch.from_numpy(yl).cuda()
+            assert O.rel_l2(outs[-1], cur.cpu().numpy()) <= GATE
+            del kept
+        st.close()
+        torch.cuda.empty_cache()
+    assert O.rel_l2(outs[1], outs[0]) <= GATE
