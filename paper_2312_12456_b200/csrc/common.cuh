@@ -163,7 +163,9 @@ __device__ __forceinline__ uint2 g_fragment(const float *gs, int ldg, const floa
       uint16_t p0[3], p1[3];
       Split3<T>::split(gb[8 * h] * sc, p0);
       Split3<T>::split(gb[8 * h + 1] * sc, p1);
-      r[h] = (uint32_t)p0[s] | ((uint32_t)p1[s] << 16);
+      const uint16_t a = s == 0 ? p0[0] : (s == 1 ? p0[1] : p0[2]);   // no dynamic register-array index
+      const uint16_t c = s == 0 ? p1[0] : (s == 1 ? p1[1] : p1[2]);
+      r[h] = (uint32_t)a | ((uint32_t)c << 16);
     }
   }
   return make_uint2(r[0], r[1]);

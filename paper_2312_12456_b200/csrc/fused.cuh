@@ -252,7 +252,9 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
         uint16_t p0[3], p1[3];
         Split3<T>::split(gv[q][2 * h] * s_b, p0);
         Split3<T>::split(gv[q][2 * h + 1] * s_b, p1);
-        r2[h] = (uint32_t)p0[s] | ((uint32_t)p1[s] << 16);
+        const uint16_t a = s == 0 ? p0[0] : (s == 1 ? p0[1] : p0[2]);   // no dynamic register-array index
+        const uint16_t c2 = s == 0 ? p1[0] : (s == 1 ? p1[1] : p1[2]);
+        r2[h] = (uint32_t)a | ((uint32_t)c2 << 16);
       }
       x.gfrag[K * 32 + L] = make_uint2(r2[0], r2[1]);
     }
@@ -543,9 +545,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
       }
       prefetch_tail(NS);
-      // speculative hot prefix: static ids, no dependency on this layer's mask -- streamed right
-      // behind the P2 stages, consumed while the grid synchronises and compacts
+      // speculative hot prefix: static ids, no dependency on this layer's mask -- streamed once this
+      // CTA's phase 2 is done (earlier they would compete with P2's own loads), consumed while the
+      // grid synchronises and compacts
       const int n_spec_c = (p.spec && lw.n_spec > c) ? (lw.n_spec - 1 - c) / P + 1 : 0;
+      if (n_spec_c) mbar_wait(p2_done, l & 1);
       for (int k0 = 0; k0 < n_spec_c; k0 += G, ++it) {
         const int kn = min(G, n_spec_c - k0);
         uint8_t *dst = acquire((uint32_t)(kn * nb));
@@ -561,7 +565,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         // CTA's phase 2 is done (its P2 stages are in, HBM idles through barrier 2 and the
         // compaction), pull this CTA's share of the first p.hot_cap of their up/down rows into
         // L2; the FFN stages of those neurons then load from L2
-        mbar_wait(p2_done, l & 1);
+        if (!n_spec_c) mbar_wait(p2_done, l & 1);
         const uint64_t keep = policy_evict_last();
         const int nh = min(lw.n_hot, p.hot_cap);
         for (int k = c; k < nh; k += P) {
@@ -825,183 +829,190 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
     };
 
-    // ---------------- grid barrier 2; with a speculative prefix it is split around the speculative stages ----------------
+    // ---------------- phase 3: every FFN stage of the layer in ONE loop (the stage code is emitted once) ----------------
+    //   stages [0, n_spec_st)          speculative hot prefix (all bits set; h saved for corrections)
+    //   -- grid barrier 2 (split-phase around the speculative stages when there are any) + compaction
+    //   stages [.., + n_st)            the cold union ids of this CTA
+    //   stages [.., + n_corr_st)       corrections: speculative neurons whose bit is 0 for some token
     const uint32_t it_spec = ring + st_p1 + st_p2;
     const int n_spec_st = (n_spec_c + G - 1) / G;
-    if (spec_on) {
-      if (tid == 0) mbar_arrive(&s_b2_arrive);   // the agent lane arrives globally and polls
-      for (int f = 0; f < n_spec_st; ++f) {
-        const int kk = f * G, kn = min(G, n_spec_c - kk);
-        if (is_up) up_stage(it_spec + f, kn, s_bspec + kk, nullptr, &s_hspec[kk]);
-        else down_stage(it_spec + f, kn);
-      }
-      mbar_wait(&s_b2_done, n_spec_layers & 1);
-      ++n_spec_layers;
-      consumers_sync();
-    } else {
-      grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
-    }
-    if (tr && tid == 0) tr[4] = globaltimer();
-
-    // ---------------- phase 3: compaction of my share ----------------
-    // One L2 round trip: all consumer threads stage the P counts, the union words and the
-    // per-token words (B > 1, or for the speculative corrections) into the ring slot the first
-    // cold FFN stage will use -- free now: every earlier stage has been consumed and the producer
-    // waits for ids_ready before reusing it.
-    const bool stage_tok = B > 1 || spec_on;
     const uint32_t it_ffn = it_spec + n_spec_st;
-    uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
-    uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (stage_tok)
-    int *c_cnt = reinterpret_cast<int *>(c_msk + (stage_tok ? B * p.words : 0));   // [P]
-    int *c_cntf = c_cnt + P;                                              // [P] (spec_on)
-    for (int i = tid; i < p.words; i += kConsumers) {
-      c_uni[i] = __ldcg(p.uni + i);
-      if (stage_tok)
-#pragma unroll
-        for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
-    }
-    if (tid < P) {
-      c_cnt[tid] = __ldcg(p.counts + tid);
-      if (spec_on) c_cntf[tid] = __ldcg(p.counts_full + tid);
-    }
-    consumers_sync();
-    if (warp == 0) {
-      // CTA-block b owns words [b W/P, (b+1) W/P)
-      constexpr int KPL = 8;  // counts per lane (P <= 256)
-      int cv[KPL];
-#pragma unroll
-      for (int i = 0; i < KPL; ++i) {
-        const int b = lane * KPL + i;
-        cv[i] = (b < P) ? c_cnt[b] : 0;
-      }
-      int lsum = 0;
-#pragma unroll
-      for (int i = 0; i < KPL; ++i) lsum += cv[i];
-      int incl = lsum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const int n = __shfl_sync(0xffffffffu, incl, 31);
-      const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
-      if (k0 < k1) {
-        int pos = incl - lsum, cand = -1, cand_before = 0;
-#pragma unroll
-        for (int i = 0; i < KPL; ++i) {
-          if (cand < 0 && pos + cv[i] > k0) {
-            cand = lane * KPL + i;
-            cand_before = pos;
-          }
-          pos += cv[i];
+    int n_mine = 0, n_corr = 0, n_st = 0, n_corr_st = 0;
+    if (spec_on && tid == 0) mbar_arrive(&s_b2_arrive);   // the agent lane arrives globally and polls
+    for (int f = 0;; ++f) {
+      if (f == n_spec_st) {
+        if (spec_on) {
+          mbar_wait(&s_b2_done, n_spec_layers & 1);
+          ++n_spec_layers;
+          consumers_sync();
+        } else {
+          grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
         }
-        const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
-        const int src = __ffs(hit) - 1;
-        const int blk = __shfl_sync(0xffffffffu, cand, src);
-        int before = __shfl_sync(0xffffffffu, cand_before, src);
-        // walk union words from the start of block blk; keep ids with position in [k0, k1)
-        int w = (int)(((int64_t)blk * p.words) / P);
-        while (before < k1 && w < p.words) {
-          const int ww = w + lane;
-          const uint32_t u = (ww < p.words) ? c_uni[ww] : 0u;
-          uint32_t bitsb[B];
-#pragma unroll
-          for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? c_msk[b * p.words + ww] : u;
-          const int cnt = __popc(u);
-          int wincl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, wincl, o);
-            if (lane >= o) wincl += t;
-          }
-          int my_pos = before + wincl - cnt;
-          uint32_t v = u;
-          while (v) {
-            const int bit = __ffs(v) - 1;
-            v &= v - 1;
-            if (my_pos >= k0 && my_pos < k1) {
-              const int slot = my_pos - k0;
-              s_ids[slot] = ww * 32 + bit;
-              uint8_t tb = 0;
-#pragma unroll
-              for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
-              s_bits[slot] = tb;
-            }
-            ++my_pos;
-          }
-          before += __shfl_sync(0xffffffffu, wincl, 31);
-          w += 32;
+        if (tr && tid == 0) tr[4] = globaltimer();
+        // ---------------- phase 3: compaction of my share ----------------
+        // One L2 round trip: all consumer threads stage the P counts, the union words and the
+        // per-token words (B > 1, or for the speculative corrections) into the ring slot the first
+        // cold FFN stage will use -- free now: every earlier stage has been consumed and the producer
+        // waits for ids_ready before reusing it.
+        const bool stage_tok = B > 1 || spec_on;
+        uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
+        uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (stage_tok)
+        int *c_cnt = reinterpret_cast<int *>(c_msk + (stage_tok ? B * p.words : 0));   // [P]
+        int *c_cntf = c_cnt + P;                                              // [P] (spec_on)
+        for (int i = tid; i < p.words; i += kConsumers) {
+          c_uni[i] = __ldcg(p.uni + i);
+          if (stage_tok)
+    #pragma unroll
+            for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
         }
-      }
-      int nfull = n;
-      if (spec_on) {   // the layer's union count includes the speculative neurons
-        int fs = 0;
-#pragma unroll
-        for (int i = 0; i < KPL; ++i) fs += (lane * KPL + i < P) ? c_cntf[lane * KPL + i] : 0;
-        nfull = __reduce_add_sync(0xffffffffu, fs);
-      }
-      if (lane == 0) {
-        s_n = nfull;
-        s_k0 = k0;
-        s_k1 = k1;
-      }
-    } else if (warp == 1) {
-      // corrections: my speculative neurons whose bit is 0 for some token (ascending k, fixed order)
-      int nc = 0;
-      for (int k0 = 0; k0 < n_spec_c; k0 += 32) {
-        const int kk = k0 + lane;
-        bool need = false;
-        uint32_t tb = 0;
-        if (kk < n_spec_c) {
-          const int i = s_spec_ids[kk];
-#pragma unroll
-          for (int b = 0; b < B; ++b) tb |= ((c_msk[b * p.words + (i >> 5)] >> (i & 31)) & 1u) << b;
-          need = tb != (1u << B) - 1u;
+        if (tid < P) {
+          c_cnt[tid] = __ldcg(p.counts + tid);
+          if (spec_on) c_cntf[tid] = __ldcg(p.counts_full + tid);
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, need);
-        if (need) {
-          const int slot = nc + __popc(bal & ((1u << lane) - 1u));
-          s_corr_ids[slot] = s_spec_ids[kk];
-#pragma unroll
-          for (int b = 0; b < B; ++b) s_corr_h[slot][b] = ((tb >> b) & 1u) ? 0.f : -s_hspec[kk][b];
-        }
-        nc += __popc(bal);
-      }
-      if (lane == 0) s_ncorr = nc;
-    }
-    // generic-proxy writes to the scratch slot before the producer's TMA overwrites it
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    consumers_sync();
-    if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
-    if (tr && tid == 0) tr[5] = globaltimer();
-    const int k0 = s_k0, n_mine = s_k1 - s_k0, n_corr = s_ncorr;
-    for (int k = tid; k < n_mine; k += kConsumers) {
-      const int i = s_ids[k];
-      s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
-      if (p.ids_out) p.ids_out[k0 + k] = i;
-    }
-    if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
-    consumers_sync();
-
-    // ---------------- phase 3: the sparse FFN over the cold ids, then the corrections ----------------
-    const int n_st = (n_mine + G - 1) / G;
-    for (int f = 0; f < n_st; ++f) {
-      const int kk = f * G, kn = min(G, n_mine - kk);
-      if (is_up) up_stage(it_ffn + f, kn, s_bup + kk, s_bits + kk, nullptr);
-      else down_stage(it_ffn + f, kn);
-    }
-    const uint32_t it_corr = it_ffn + n_st;
-    const int n_corr_st = (n_corr + G - 1) / G;
-    for (int f = 0; f < n_corr_st; ++f) {
-      const uint32_t it = it_corr + f;
-      const int kk = f * G, kn = min(G, n_corr - kk);
-      if (is_up) {
-        // h of a correction = minus the speculative h of each token whose bit is 0 (0 otherwise)
-        wait_full(it);
+        consumers_sync();
         if (warp == 0) {
-          if (lane < kn * B) hs[(it % NS) * (NA * B) + lane] = s_corr_h[kk + lane / B][lane % B];
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&hready[it % NS]);
+          // CTA-block b owns words [b W/P, (b+1) W/P)
+          constexpr int KPL = 8;  // counts per lane (P <= 256)
+          int cv[KPL];
+    #pragma unroll
+          for (int i = 0; i < KPL; ++i) {
+            const int b = lane * KPL + i;
+            cv[i] = (b < P) ? c_cnt[b] : 0;
+          }
+          int lsum = 0;
+    #pragma unroll
+          for (int i = 0; i < KPL; ++i) lsum += cv[i];
+          int incl = lsum;
+    #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+          }
+          const int n = __shfl_sync(0xffffffffu, incl, 31);
+          const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
+          if (k0 < k1) {
+            int pos = incl - lsum, cand = -1, cand_before = 0;
+    #pragma unroll
+            for (int i = 0; i < KPL; ++i) {
+              if (cand < 0 && pos + cv[i] > k0) {
+                cand = lane * KPL + i;
+                cand_before = pos;
+              }
+              pos += cv[i];
+            }
+            const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
+            const int src = __ffs(hit) - 1;
+            const int blk = __shfl_sync(0xffffffffu, cand, src);
+            int before = __shfl_sync(0xffffffffu, cand_before, src);
+            // walk union words from the start of block blk; keep ids with position in [k0, k1)
+            int w = (int)(((int64_t)blk * p.words) / P);
+            while (before < k1 && w < p.words) {
+              const int ww = w + lane;
+              const uint32_t u = (ww < p.words) ? c_uni[ww] : 0u;
+              uint32_t bitsb[B];
+    #pragma unroll
+              for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? c_msk[b * p.words + ww] : u;
+              const int cnt = __popc(u);
+              int wincl = cnt;
+    #pragma unroll
+              for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, wincl, o);
+                if (lane >= o) wincl += t;
+              }
+              int my_pos = before + wincl - cnt;
+              uint32_t v = u;
+              while (v) {
+                const int bit = __ffs(v) - 1;
+                v &= v - 1;
+                if (my_pos >= k0 && my_pos < k1) {
+                  const int slot = my_pos - k0;
+                  s_ids[slot] = ww * 32 + bit;
+                  uint8_t tb = 0;
+    #pragma unroll
+                  for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
+                  s_bits[slot] = tb;
+                }
+                ++my_pos;
+              }
+              before += __shfl_sync(0xffffffffu, wincl, 31);
+              w += 32;
+            }
+          }
+          int nfull = n;
+          if (spec_on) {   // the layer's union count includes the speculative neurons
+            int fs = 0;
+    #pragma unroll
+            for (int i = 0; i < KPL; ++i) fs += (lane * KPL + i < P) ? c_cntf[lane * KPL + i] : 0;
+            nfull = __reduce_add_sync(0xffffffffu, fs);
+          }
+          if (lane == 0) {
+            s_n = nfull;
+            s_k0 = k0;
+            s_k1 = k1;
+          }
+        } else if (warp == 1) {
+          // corrections: my speculative neurons whose bit is 0 for some token (ascending k, fixed order)
+          int nc = 0;
+          for (int k0 = 0; k0 < n_spec_c; k0 += 32) {
+            const int kk = k0 + lane;
+            bool need = false;
+            uint32_t tb = 0;
+            if (kk < n_spec_c) {
+              const int i = s_spec_ids[kk];
+    #pragma unroll
+              for (int b = 0; b < B; ++b) tb |= ((c_msk[b * p.words + (i >> 5)] >> (i & 31)) & 1u) << b;
+              need = tb != (1u << B) - 1u;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, need);
+            if (need) {
+              const int slot = nc + __popc(bal & ((1u << lane) - 1u));
+              s_corr_ids[slot] = s_spec_ids[kk];
+    #pragma unroll
+              for (int b = 0; b < B; ++b) s_corr_h[slot][b] = ((tb >> b) & 1u) ? 0.f : -s_hspec[kk][b];
+            }
+            nc += __popc(bal);
+          }
+          if (lane == 0) s_ncorr = nc;
+        }
+        // generic-proxy writes to the scratch slot before the producer's TMA overwrites it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        consumers_sync();
+        if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
+        if (tr && tid == 0) tr[5] = globaltimer();
+        {
+          const int k0 = s_k0;
+          n_mine = s_k1 - s_k0;
+          n_corr = s_ncorr;
+          for (int k = tid; k < n_mine; k += kConsumers) {
+            const int i = s_ids[k];
+            s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
+            if (p.ids_out) p.ids_out[k0 + k] = i;
+          }
+        }
+        if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
+        consumers_sync();
+
+        n_st = (n_mine + G - 1) / G;
+        n_corr_st = (n_corr + G - 1) / G;
+      }
+      if (f >= n_spec_st + n_st + n_corr_st) break;
+      const uint32_t it = it_spec + f;
+      const int fs = f - n_spec_st, fc = fs - n_st;   // index among the cold / correction stages
+      const int kk = (fs < 0 ? f : fc < 0 ? fs : fc) * G;
+      const int kn = min(G, (fs < 0 ? n_spec_c : fc < 0 ? n_mine : n_corr) - kk);
+      if (is_up) {
+        if (fs < 0) {
+          up_stage(it, kn, s_bspec + kk, nullptr, &s_hspec[kk]);
+        } else if (fc < 0) {
+          up_stage(it, kn, s_bup + kk, s_bits + kk, nullptr);
+        } else {
+          // h of a correction = minus the speculative h of each token whose bit is 0 (0 otherwise)
+          wait_full(it);
+          if (warp == 0) {
+            if (lane < kn * B) hs[(it % NS) * (NA * B) + lane] = s_corr_h[kk + lane / B][lane % B];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hready[it % NS]);
+          }
         }
       } else {
         down_stage(it, kn);
@@ -1022,7 +1033,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         }
       }
     }
-    ring = it_corr + n_corr_st;
+    ring = it_ffn + n_st + n_corr_st;
 
     if (tr && tid == 0) tr[6] = globaltimer();
     grid_sync(p.bar, P, tr ? tr + 208 : nullptr);
@@ -1089,7 +1100,7 @@ cudaError_t fused_launch_tbr(const FusedWork &w, const FusedParams &p, int CH, i
   if (CH == CHV && NA == NAV) return fused_launch_t<T, B, RG, CHV, NAV>(w, p, s);
   PI_FL(1, 8) PI_FL(1, 1) PI_FL(2, 8) PI_FL(2, 1) PI_FL(3, 1) PI_FL(4, 1)
   if constexpr (B == 1) {   // wider d keeps x and y register-resident only for one token
-    PI_FL(6, 1) PI_FL(8, 1)
+    PI_FL(5, 1) PI_FL(6, 1) PI_FL(7, 1) PI_FL(8, 1)
   }
 #undef PI_FL
   return cudaErrorNotSupported;

@@ -39,7 +39,7 @@
 
 namespace pi {
 
-constexpr int kGroupWarps = 8;                        // warps per group (up / down)
+constexpr int kGroupWarps = 7;                        // warps per group (up / down)
 constexpr int kGroup = kGroupWarps * 32;              // 256 threads per group
 constexpr int kConsumerWarps = 2 * kGroupWarps;       // 16
 constexpr int kConsumers = kConsumerWarps * 32;       // 512
@@ -129,7 +129,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.r = r;
   w.reglu = reglu;
   const int ch = fused_ch(d);
-  if (ch > kMaxCH || ch == 5 || ch == 7 || d < 8 || r > 16 * num_sms || num_sms > 256)
+  if (ch > kMaxCH || d < 8 || r > 16 * num_sms || num_sms > 256)
     return true;  // unsupported shape: stays disabled (per-step kernels)
   w.P = num_sms;
   w.kt = (r + 15) / 16;
@@ -197,9 +197,9 @@ inline bool fused_supported(const FusedWork &w, int B = 1) {
   if (ch * 8 * B > 64) return false;  // register-resident x / y per group thread
   int NA, G, RP1;
   fused_geometry(w, w.d, w.reglu, &NA, &G, &RP1);
-  // the instantiated (CH, NA) combinations (fused_launch)
+  // the instantiated (CH, NA) combinations (fused_launch_tbr)
   if (ch <= 2) return true;
-  return NA == 1 && (ch == 3 || ch == 4 || (B == 1 && (ch == 6 || ch == 8)));
+  return NA == 1 && (ch <= 4 || (B == 1 && ch <= kMaxCH));
 }
 
 // One instantiation unit per (weight type, batch, activation): fused_inst_<T>_b<B>_<act>.cu

@@ -146,7 +146,7 @@ class Layer:
     def __init__(self, w, neuron_ids: Optional[Sequence[int]] = None, max_batch: int = 1, flags: int = 0,
                  layer_id: int = 0, threshold: Optional[float] = None, pred_act: Optional[str] = None,
                  own_b_down: bool = True, stream=None, neuron_freq=None, hot_freq: float = 0.9,
-                 hot_cap: int = 0, q4=None, spec_freq: float = 0.0, spec_cap: int = 0):
+                 hot_cap: int = 0, q4=None, spec_freq: float = 0.0, spec_cap: int = 1 << 30):
         """w: gen.LayerWeights (16-bit global tensors).  q4: optional gen.Q4Weights -- the FFN
         then runs on INT4 neuron rows (PI_FFN_Q4); w still supplies the predictor and biases."""
         self.handle = None
