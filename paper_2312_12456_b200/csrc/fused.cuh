@@ -185,8 +185,8 @@ struct P2Ctx {
   uint64_t *full, *empty, *hready;
   volatile uint32_t *slot_pos;   // [NS] ring position the producer last acquired each slot for
   float *zbuf, *s_b2;
-  int *s_count, *s_count_full;   // this CTA's union counts: without / with the speculative neurons
-  const uint32_t *spec_words;    // speculative-neuron bitmap (NULL: none); cleared from the union words
+  int *s_count, *s_count_full;   // union counts without / with the speculative neurons (SPEC)
+  const uint32_t *spec_words;    // speculative-neuron bitmap (SPEC); cleared from the union words
   uint2 *gfrag;                  // [kt][NT][32] shared B fragments
   unsigned *gmax;                // [B] shared max |g| bits (fp16 scaling), zeroed at layer start
   unsigned long long *trace;
@@ -197,7 +197,7 @@ struct P2Ctx {
   uint32_t *mask, *uni;
 };
 
-template <typename T, int B>
+template <typename T, int B, bool SPEC>
 __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   constexpr int NT = (3 * B + 7) / 8;
   static_assert(NT == 1, "fused phase 2 handles B <= 2 (one n tile)");
@@ -335,8 +335,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
   }
   consumers_sync();   // every logit of this CTA's words is in zbuf
   if (dt && warp == 0) dt[3] = globaltimer();
-  // ballots: one warp per mask word -> per-token words, union word (without the speculative
-  // neurons, which are computed before the compaction), popcounts
+  // ballots: one warp per mask word -> per-token words, union word, popcount
   int my_count = 0, my_full = 0;
   for (int wl = warp; wl < x.w1 - x.w0; wl += kConsumerWarps) {
     const int rl = wl * 32 + lane;
@@ -351,14 +350,14 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       if (lane == 0) x.mask[(size_t)b * x.words + x.w0 + wl] = bits;
     }
     if (lane == 0) {
-      const uint32_t uc = x.spec_words ? (u & ~x.spec_words[x.w0 + wl]) : u;
+      const uint32_t uc = (SPEC && x.spec_words) ? (u & ~x.spec_words[x.w0 + wl]) : u;
       x.uni[x.w0 + wl] = uc;
       my_count += __popc(uc);
-      my_full += __popc(u);
+      if (SPEC) my_full += __popc(u);
     }
   }
   if (lane == 0 && my_count) atomicAdd(x.s_count, my_count);
-  if (lane == 0 && my_full) atomicAdd(x.s_count_full, my_full);
+  if (SPEC && lane == 0 && my_full) atomicAdd(x.s_count_full, my_full);
   if (x.trace && tid == 0) x.trace[3] = globaltimer();
 }
 
@@ -367,7 +366,57 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
 //   CH : 16-byte chunks of d per group thread (chunk = t + 256 q, q < CH)
 //   NA : max neurons per ring stage (also bounds P1 rows per stage: NA == 1 -> 2, else 8)
 // ---------------------------------------------------------------------------
-template <typename T, int B, bool REGLU, int CH, int NA>
+// the first argument if S, else the second (references to arrays of the same type)
+template <bool S, class A, class Bb>
+__device__ __forceinline__ auto &pick(A &a, Bb &b) {
+  if constexpr (S) return a;
+  else return b;
+}
+
+// this CTA's partial y (register-resident, down group) -> global [B][d]
+template <int B, int CH>
+__device__ __forceinline__ void store_partial(const float (&yr)[CH][8][B], float *dst0, int d, int gt, int chunks) {
+#pragma unroll
+  for (int q = 0; q < CH; ++q) {
+    const int ch = gt + q * kGroup;
+    if (ch < chunks) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        float4 *dst = reinterpret_cast<float4 *>(dst0 + (size_t)b * d + ch * 8);
+        __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
+        __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
+      }
+    }
+  }
+}
+
+// SPEC: one down-group FFN stage: y_part += h * down row for the stage's kn neurons
+template <typename T, int B, int CH, int NA>
+__device__ __forceinline__ void spec_down_stage(float (&yr)[CH][8][B], const uint8_t *buf, const float *hh, int kn,
+                                                size_t nb, size_t row_up, int gt, int chunks) {
+#pragma unroll
+  for (int g = 0; g < NA; ++g) {
+    float h[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
+    const size_t go = (size_t)g * nb + row_up;
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const int ch = gt + q * kGroup;
+      float wf[8];
+      WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
+    }
+  }
+}
+
+// SPEC variant: see k_layer below
+// SPEC: the speculative hot prefix (pi_layer_desc.spec_freq) -- a separate instantiation, so the
+// default kernel carries none of its code (it costs registers: measured slower).
+template <typename T, int B, bool REGLU, int CH, int NA, bool SPEC>
 __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p) {
   constexpr int RPM = (NA == 1) ? 2 : 8;      // max P1 rows per stage
   extern __shared__ __align__(128) uint8_t fsmem[];
@@ -396,14 +445,14 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
   __shared__ unsigned s_gmax[B];
   __shared__ uint32_t s_slot_pos[kMaxStages];
-  // speculative hot prefix (this CTA's share) and its corrections
-  __shared__ int32_t s_spec_ids[kMaxSpecPerCta];
-  __shared__ float s_bspec[kMaxSpecPerCta];
-  __shared__ float s_hspec[kMaxSpecPerCta][B];
-  __shared__ int32_t s_corr_ids[kMaxCorrPerCta];
-  __shared__ float s_corr_h[kMaxCorrPerCta][B];
+  // SPEC: this CTA's share of the speculative hot prefix and its corrections
+  __shared__ int32_t s_spec_ids[SPEC ? kMaxSpecPerCta : 1];
+  __shared__ float s_bspec[SPEC ? kMaxSpecPerCta : 1];
+  __shared__ float s_hspec[SPEC ? kMaxSpecPerCta : 1][B];
+  __shared__ int32_t s_corr_ids[SPEC ? kMaxCorrPerCta : 1];
+  __shared__ float s_corr_h[SPEC ? kMaxCorrPerCta : 1][B];
   __shared__ int s_ncorr, s_count_full;
-  __shared__ __align__(8) uint64_t s_b2_arrive, s_b2_done;   // split-phase grid barrier 2
+  __shared__ __align__(8) uint64_t s_b2_arrive, s_b2_done;   // SPEC: split-phase grid barrier 2
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[16];
   __shared__ int s_n, s_k0, s_k1, s_count;
@@ -447,31 +496,33 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   // rows while the consumers finish the current layer (bounded by the ring)
   // =====================================================================================
   if (warp == kConsumerWarps) {
-    if (lane == 1) {
-      // barrier agent: grid barrier 2 of layers with a speculative prefix is split -- the
-      // consumers signal their arrival and go on computing the speculative neurons while this
-      // lane does the global arrive and poll, then releases them through s_b2_done
-      int ns = 0;
-      for (int l = 0; l < L; ++l) {
-        if (!(p.spec && layer(l).n_spec > 0)) continue;
-        mbar_wait(&s_b2_arrive, ns & 1);
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        unsigned long long old;
-        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.bar) : "memory");
-        const unsigned long long target = (old / (unsigned long long)P + 1ull) * (unsigned long long)P;
-        const unsigned long long t0 = globaltimer();
-        while (true) {
-          unsigned long long cur;
-          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(p.bar) : "memory");
-          if (cur >= target) break;
-          __nanosleep(32);
-          if (globaltimer() - t0 > 4000000000ull) __trap();
+    if constexpr (SPEC) {
+      if (lane == 1) {
+        // barrier agent: grid barrier 2 of layers with a speculative prefix is split -- the
+        // consumers signal their arrival and compute the speculative neurons while this lane does
+        // the global arrive and poll, then releases them through s_b2_done
+        int ns = 0;
+        for (int l = 0; l < L; ++l) {
+          if (layer(l).n_spec <= 0) continue;
+          mbar_wait(&s_b2_arrive, ns & 1);
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          unsigned long long old;
+          asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(p.bar) : "memory");
+          const unsigned long long target = (old / (unsigned long long)P + 1ull) * (unsigned long long)P;
+          const unsigned long long t0 = globaltimer();
+          while (true) {
+            unsigned long long cur;
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(p.bar) : "memory");
+            if (cur >= target) break;
+            __nanosleep(32);
+            if (globaltimer() - t0 > 4000000000ull) __trap();
+          }
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          mbar_arrive(&s_b2_done);
+          ++ns;
         }
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        mbar_arrive(&s_b2_done);
-        ++ns;
+        return;
       }
-      return;
     }
     if (lane != 0) return;
     const uint64_t pol = policy_evict_first();
@@ -545,19 +596,21 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         bulk_g2s(dst, lw.p_w2 + (size_t)ra * rowb2, bytes, &full[it % NS], pol);
       }
       prefetch_tail(NS);
-      // speculative hot prefix: static ids, no dependency on this layer's mask -- streamed once this
-      // CTA's phase 2 is done (earlier they would compete with P2's own loads), consumed while the
-      // grid synchronises and compacts
-      const int n_spec_c = (p.spec && lw.n_spec > c) ? (lw.n_spec - 1 - c) / P + 1 : 0;
-      if (n_spec_c) mbar_wait(p2_done, l & 1);
-      for (int k0 = 0; k0 < n_spec_c; k0 += G, ++it) {
-        const int kn = min(G, n_spec_c - k0);
-        uint8_t *dst = acquire((uint32_t)(kn * nb));
-        const int s = it % NS;
-        for (int k = 0; k < kn; ++k) {
-          const int i = lw.spec_ids[c + (k0 + k) * P];
-          bulk_g2s(dst + (size_t)k * nb, lw.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
-          bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+      int n_spec_c = 0;
+      if constexpr (SPEC) {
+        // speculative hot prefix: static ids, no dependency on this layer's mask -- streamed once
+        // this CTA's phase 2 is done, consumed while the grid synchronises and compacts
+        n_spec_c = lw.n_spec > c ? (lw.n_spec - 1 - c) / P + 1 : 0;
+        if (n_spec_c) mbar_wait(p2_done, l & 1);
+        for (int k0 = 0; k0 < n_spec_c; k0 += G, ++it) {
+          const int kn = min(G, n_spec_c - k0);
+          uint8_t *dst = acquire((uint32_t)(kn * nb));
+          const int s = it % NS;
+          for (int k = 0; k < kn; ++k) {
+            const int i = lw.spec_ids[c + (k0 + k) * P];
+            bulk_g2s(dst + (size_t)k * nb, lw.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
+            bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+          }
         }
       }
       if (lw.n_hot) {
@@ -586,15 +639,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
         }
       }
-      // corrections of speculative neurons whose bit is 0 for some token: their down rows again
-      const int n_corr = s_ncorr;
-      for (int k0 = 0; k0 < n_corr; k0 += G, ++it) {
-        const int kn = min(G, n_corr - k0);
-        uint8_t *dst = acquire((uint32_t)(kn * row_dn));
-        const int s = it % NS;
-        for (int k = 0; k < kn; ++k) {
-          const int i = s_corr_ids[k0 + k];
-          bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+      if constexpr (SPEC) {
+        // corrections of speculative neurons whose bit is 0 for some token: their down rows again
+        const int n_corr = s_ncorr;
+        for (int k0 = 0; k0 < n_corr; k0 += G, ++it) {
+          const int kn = min(G, n_corr - k0);
+          uint8_t *dst = acquire((uint32_t)(kn * row_dn));
+          const int s = it % NS;
+          for (int k = 0; k < kn; ++k) {
+            const int i = s_corr_ids[k0 + k];
+            bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+          }
         }
       }
     }
@@ -611,7 +666,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   const int gw = gt >> 5;                      // warp index inside its group
   auto stage_ptr = [&](uint32_t it) { return stages + (size_t)(it % NS) * SB; };
   uint32_t ring = 0;                           // ring position of this layer's first stage
-  int n_spec_layers = 0;                       // layers with a speculative prefix so far (s_b2_* parity)
+  int n_spec_layers = 0;                       // SPEC: layers with a speculative prefix so far (s_b2_* parity)
 
   for (int l = 0; l < L; ++l) {
     const LayerW lw = layer(l);
@@ -629,15 +684,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       s_ncorr = 0;
     }
     if (tid < B) s_gmax[tid] = 0u;
-    // this CTA's share of the speculative hot prefix: neurons c, c + P, ... of the layer's list
-    const bool spec_on = p.spec && lw.n_spec > 0;
-    const int n_spec_c = spec_on && lw.n_spec > c ? (lw.n_spec - 1 - c) / P + 1 : 0;
-    for (int k = tid; k < n_spec_c; k += kConsumers) {
-      const int i = lw.spec_ids[c + k * P];
-      s_spec_ids[k] = i;
-      s_bspec[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
-    }
     if (tr && tid == 0) tr[0] = globaltimer();
+    // SPEC: this CTA's share of the speculative hot prefix: neurons c, c + P, ... of the layer's list
+    const bool spec_on = SPEC && lw.n_spec > 0;
+    const int n_spec_c = spec_on && lw.n_spec > c ? (lw.n_spec - 1 - c) / P + 1 : 0;
+    if constexpr (SPEC) {
+      for (int k = tid; k < n_spec_c; k += kConsumers) {
+        const int i = lw.spec_ids[c + k * P];
+        s_spec_ids[k] = i;
+        s_bspec[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
+      }
+    }
 
     float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
     float sc[B];
@@ -732,306 +789,366 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       P2Ctx ctx{stages, full, empty, hready, s_slot_pos, zbuf, s_b2, &s_count, &s_count_full,
                 spec_on ? lw.spec_words : nullptr, gfrag, s_gmax, tr, NS, SB, (int)ring + st_p1, st_p2, w0, w1, m,
                 r, p.kt, p.words, p.words_p2, p.wcap * 32, ring, lw.t, p.g, p.mask, p.uni};
-      p2_phase<T, B>(ctx);
+      p2_phase<T, B, SPEC>(ctx);
     }
     consumers_sync();
     if (tid == 0) {
       p.counts[c] = s_count;
-      p.counts_full[c] = s_count_full;
+      if (SPEC) p.counts_full[c] = s_count_full;
       mbar_arrive(p2_done);
     }
+    // down group: the partial y lives in yr; SPEC keeps it from the speculative stages on (outer
+    // scope), the default kernel declares it where the FFN starts (a longer live range costs spills)
+    float yrs[SPEC ? CH : 1][8][B];
+    const uint32_t it_spec = ring + st_p1 + st_p2;
+    const int n_spec_st = (n_spec_c + G - 1) / G;
+    if constexpr (SPEC) {
+      if (spec_on) {
+        auto ffn_up_stage = [&](uint32_t it, int kn, const float *bup_s, const uint8_t *bits_s, float (*hsave)[B]) {
+          constexpr int NV = NA * B * (REGLU ? 2 : 1);
+          wait_full(it);
+          const uint8_t *buf = stage_ptr(it);
+          float acc[NV];
+#pragma unroll
+          for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+#pragma unroll
+          for (int g = 0; g < NA; ++g) {
+            const size_t go = (size_t)g * nb;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const int ch = gt + q * kGroup;
+              const bool ok = g < kn && ch < chunks;
+              float wu[8];
+              if (REGLU) {
+                float wg[8];
+                WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
+                WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+#pragma unroll
+                  for (int e = 0; e < 8; ++e)
+                    acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+              } else {
+                WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
+              }
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+                  acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+                }
+            }
+          }
+          float *rb = red + (it & 1) * kGroupWarps * kRedStride;
+          up_partials<NV>(acc, rb);
+          if (warp == 0) {
+            if (lane < kn * B) {
+              const int g = lane / B, b = lane % B;
+              const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + bup_s[g];
+              const float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
+              hs[(it % NS) * (NA * B) + lane] = (!bits_s || ((bits_s[g] >> b) & 1)) ? hv : 0.f;
+              if (hsave) hsave[g][b] = hv;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hready[it % NS]);
+          }
+        };
+        if (tid == 0) mbar_arrive(&s_b2_arrive);   // the agent lane arrives globally and polls
+        if (!is_up) {
+#pragma unroll
+          for (int q = 0; q < CH; ++q)
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+#pragma unroll
+              for (int b = 0; b < B; ++b) yrs[q][e][b] = 0.f;
+        }
+        for (int f = 0; f < n_spec_st; ++f) {
+          const uint32_t it = it_spec + f;
+          const int kk = f * G, kn = min(G, n_spec_c - kk);
+          if (is_up) {
+            ffn_up_stage(it, kn, s_bspec + kk, nullptr, &s_hspec[kk]);
+          } else {
+            wait_full(it);
+            mbar_wait(&hready[it % NS], (it / NS) & 1);
+            spec_down_stage<T, B, CH, NA>(pick<SPEC>(yrs, yrs), stage_ptr(it), hs + (it % NS) * (NA * B), kn, nb,
+                                          row_up, gt, chunks);
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
+          }
+        }
+        mbar_wait(&s_b2_done, n_spec_layers & 1);
+        ++n_spec_layers;
+        consumers_sync();
+      } else {
+        grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
+      }
+    } else {
+      grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
+    }
+    if (tr && tid == 0) tr[4] = globaltimer();
 
-    // ---------------- FFN stage processing (shared by the speculative, cold and correction stages) ----------------
-    //   up group  : up (and gate) dots of the stage's kn neurons, h = act(.) -> hs (+ hsave)
-    //   down group: y_part += h * down row (register-resident partial y)
-    float yr[CH][8][B];
+    // ---------------- phase 3: compaction of my share ----------------
+    // One L2 round trip: all consumer threads stage the P counts, the union words and (B > 1)
+    // the per-token words into the ring slot the first FFN stage will use -- free now: every
+    // predictor stage has been consumed and the producer waits for ids_ready before reusing it.
+    const uint32_t it_ffn = it_spec + n_spec_st;
+    const bool stage_tok = B > 1 || spec_on;                             // per-token words staged
+    uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
+    uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (stage_tok)
+    int *c_cnt = reinterpret_cast<int *>(c_msk + (stage_tok ? B * p.words : 0));   // [P]
+    int *c_cntf = c_cnt + P;                                              // [P] (SPEC)
+    for (int i = tid; i < p.words; i += kConsumers) {
+      c_uni[i] = __ldcg(p.uni + i);
+      if (stage_tok)
 #pragma unroll
-    for (int q = 0; q < CH; ++q)
+        for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
+    }
+    if (tid < P) {
+      c_cnt[tid] = __ldcg(p.counts + tid);
+      if (SPEC && spec_on) c_cntf[tid] = __ldcg(p.counts_full + tid);
+    }
+    consumers_sync();
+    if (warp == 0) {
+      // CTA-block b owns words [b W/P, (b+1) W/P)
+      constexpr int KPL = 8;  // counts per lane (P <= 256)
+      int cv[KPL];
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
+      for (int i = 0; i < KPL; ++i) {
+        const int b = lane * KPL + i;
+        cv[i] = (b < P) ? c_cnt[b] : 0;
+      }
+      int lsum = 0;
 #pragma unroll
-        for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
-    // bup_s[g] = b_up of the stage's g-th neuron; bits_s[g] = its per-token bits (NULL: all set);
-    // hsave[g][b] receives h (speculative stages)
-    auto up_stage = [&](uint32_t it, int kn, const float *bup_s, const uint8_t *bits_s, float (*hsave)[B]) {
+      for (int i = 0; i < KPL; ++i) lsum += cv[i];
+      int incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int n = __shfl_sync(0xffffffffu, incl, 31);
+      const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
+      if (k0 < k1) {
+        int pos = incl - lsum, cand = -1, cand_before = 0;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) {
+          if (cand < 0 && pos + cv[i] > k0) {
+            cand = lane * KPL + i;
+            cand_before = pos;
+          }
+          pos += cv[i];
+        }
+        const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
+        const int src = __ffs(hit) - 1;
+        const int blk = __shfl_sync(0xffffffffu, cand, src);
+        int before = __shfl_sync(0xffffffffu, cand_before, src);
+        // walk union words from the start of block blk; keep ids with position in [k0, k1)
+        int w = (int)(((int64_t)blk * p.words) / P);
+        while (before < k1 && w < p.words) {
+          const int ww = w + lane;
+          const uint32_t u = (ww < p.words) ? c_uni[ww] : 0u;
+          uint32_t bitsb[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? c_msk[b * p.words + ww] : u;
+          const int cnt = __popc(u);
+          int wincl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, wincl, o);
+            if (lane >= o) wincl += t;
+          }
+          int my_pos = before + wincl - cnt;
+          uint32_t v = u;
+          while (v) {
+            const int bit = __ffs(v) - 1;
+            v &= v - 1;
+            if (my_pos >= k0 && my_pos < k1) {
+              const int slot = my_pos - k0;
+              s_ids[slot] = ww * 32 + bit;
+              uint8_t tb = 0;
+#pragma unroll
+              for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
+              s_bits[slot] = tb;
+            }
+            ++my_pos;
+          }
+          before += __shfl_sync(0xffffffffu, wincl, 31);
+          w += 32;
+        }
+      }
+      int nfull = n;
+      if (SPEC && spec_on) {   // the layer's union count includes the speculative neurons
+        int fs = 0;
+#pragma unroll
+        for (int i = 0; i < KPL; ++i) fs += (lane * KPL + i < P) ? c_cntf[lane * KPL + i] : 0;
+        nfull = __reduce_add_sync(0xffffffffu, fs);
+      }
+      if (lane == 0) {
+        s_n = nfull;
+        s_k0 = k0;
+        s_k1 = k1;
+      }
+    } else if (SPEC && warp == 1) {
+      // corrections: my speculative neurons whose bit is 0 for some token (ascending k, fixed order)
+      int nc = 0;
+      for (int kb = 0; kb < n_spec_c; kb += 32) {
+        const int kk = kb + lane;
+        bool need = false;
+        uint32_t tb = 0;
+        if (kk < n_spec_c) {
+          const int i = s_spec_ids[kk];
+#pragma unroll
+          for (int b = 0; b < B; ++b) tb |= ((c_msk[b * p.words + (i >> 5)] >> (i & 31)) & 1u) << b;
+          need = tb != (1u << B) - 1u;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, need);
+        if (need) {
+          const int slot = nc + __popc(bal & ((1u << lane) - 1u));
+          s_corr_ids[slot] = s_spec_ids[kk];
+#pragma unroll
+          for (int b = 0; b < B; ++b) s_corr_h[slot][b] = ((tb >> b) & 1u) ? 0.f : -s_hspec[kk][b];
+        }
+        nc += __popc(bal);
+      }
+      if (lane == 0) s_ncorr = nc;
+    }
+    // generic-proxy writes to the scratch slot before the producer's TMA overwrites it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    consumers_sync();
+    if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
+    if (tr && tid == 0) tr[5] = globaltimer();
+    const int k0 = s_k0, n_mine = s_k1 - s_k0;
+    for (int k = tid; k < n_mine; k += kConsumers) {
+      const int i = s_ids[k];
+      s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
+      if (p.ids_out) p.ids_out[k0 + k] = i;
+    }
+    if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
+    consumers_sync();
+
+    // ---------------- phase 3: the sparse FFN ----------------
+    const int n_st = (n_mine + G - 1) / G;
+    if (is_up) {
       constexpr int NV = NA * B * (REGLU ? 2 : 1);
-      wait_full(it);
-      const uint8_t *buf = stage_ptr(it);
-      float acc[NV];
+      for (int f = 0; f < n_st; ++f) {
+        const uint32_t it = it_ffn + f;
+        const int kk = f * G, kn = min(G, n_mine - kk);
+        wait_full(it);
+        const uint8_t *buf = stage_ptr(it);
+        float acc[NV];
 #pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] = 0.f;
+        for (int i = 0; i < NV; ++i) acc[i] = 0.f;
 #pragma unroll
-      for (int g = 0; g < NA; ++g) {
-        const size_t go = (size_t)g * nb;
+        for (int g = 0; g < NA; ++g) {
+          const size_t go = (size_t)g * nb;
 #pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
-          const bool ok = g < kn && ch < chunks;
-          float wu[8];
-          if (REGLU) {
-            float wg[8];
-            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
-            WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            const bool ok = g < kn && ch < chunks;
+            float wu[8];
+            if (REGLU) {
+              float wg[8];
+              WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wg);
+              WT<T>::unpack(lds128z(buf, go + (size_t)d * 2 + (size_t)ch * 16, ok), wu);
+#pragma unroll
+              for (int b = 0; b < B; ++b)
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+            } else {
+              WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
+            }
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
-              for (int e = 0; e < 8; ++e)
-                acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
-          } else {
-            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
+              for (int e = 0; e < 8; ++e) {
+                const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
+                acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+              }
           }
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-              acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
-            }
+        }
+        float *rb = red + (f & 1) * kGroupWarps * kRedStride;
+        up_partials<NV>(acc, rb);
+        if (warp == 0) {
+          if (lane < kn * B) {
+            const int g = lane / B, b = lane % B;
+            const int slot = kk + g;
+            const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + s_bup[slot];
+            float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
+            hs[(it % NS) * (NA * B) + lane] = ((s_bits[slot] >> b) & 1) ? hv : 0.f;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hready[it % NS]);
         }
       }
-      float *rb = red + (it & 1) * kGroupWarps * kRedStride;
-      up_partials<NV>(acc, rb);
-      if (warp == 0) {
-        if (lane < kn * B) {
-          const int g = lane / B, b = lane % B;
-          const float a = (REGLU ? up_total(rb, 2 * lane) : up_total(rb, lane)) * sc[b] + bup_s[g];
-          const float hv = REGLU ? fmaxf(up_total(rb, 2 * lane + 1) * sc[b], 0.f) * a : fmaxf(a, 0.f);
-          hs[(it % NS) * (NA * B) + lane] = (!bits_s || ((bits_s[g] >> b) & 1)) ? hv : 0.f;
-          if (hsave) hsave[g][b] = hv;
+    } else {
+      float yl[SPEC ? 1 : CH][8][B];
+      float(&yr)[CH][8][B] = pick<SPEC>(yrs, yl);
+      if (!spec_on) {
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+#pragma unroll
+            for (int b = 0; b < B; ++b) yr[q][e][b] = 0.f;
+      }
+      for (int f = 0; f < n_st; ++f) {
+        const uint32_t it = it_ffn + f;
+        const int kn = min(G, n_mine - f * G);
+        wait_full(it);
+        mbar_wait(&hready[it % NS], (it / NS) & 1);
+        const uint8_t *buf = stage_ptr(it);
+        const float *hh = hs + (it % NS) * (NA * B);
+#pragma unroll
+        for (int g = 0; g < NA; ++g) {
+          float h[B];
+#pragma unroll
+          for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
+          const size_t go = (size_t)g * nb + row_up;
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const int ch = gt + q * kGroup;
+            float wf[8];
+            WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
+#pragma unroll
+            for (int b = 0; b < B; ++b)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
+          }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&hready[it % NS]);
+        if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
       }
-    };
-    auto down_stage = [&](uint32_t it, int kn) {
-      wait_full(it);
-      mbar_wait(&hready[it % NS], (it / NS) & 1);
-      const uint8_t *buf = stage_ptr(it);
-      const float *hh = hs + (it % NS) * (NA * B);
-#pragma unroll
-      for (int g = 0; g < NA; ++g) {
-        float h[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
-        const size_t go = (size_t)g * nb + row_up;
-#pragma unroll
-        for (int q = 0; q < CH; ++q) {
-          const int ch = gt + q * kGroup;
-          float wf[8];
-          WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, g < kn && ch < chunks), wf);
-#pragma unroll
-          for (int b = 0; b < B; ++b)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) yr[q][e][b] = fmaf(h[b], wf[e], yr[q][e][b]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
-    };
-
-    // ---------------- phase 3: every FFN stage of the layer in ONE loop (the stage code is emitted once) ----------------
-    //   stages [0, n_spec_st)          speculative hot prefix (all bits set; h saved for corrections)
-    //   -- grid barrier 2 (split-phase around the speculative stages when there are any) + compaction
-    //   stages [.., + n_st)            the cold union ids of this CTA
-    //   stages [.., + n_corr_st)       corrections: speculative neurons whose bit is 0 for some token
-    const uint32_t it_spec = ring + st_p1 + st_p2;
-    const int n_spec_st = (n_spec_c + G - 1) / G;
-    const uint32_t it_ffn = it_spec + n_spec_st;
-    int n_mine = 0, n_corr = 0, n_st = 0, n_corr_st = 0;
-    if (spec_on && tid == 0) mbar_arrive(&s_b2_arrive);   // the agent lane arrives globally and polls
-    for (int f = 0;; ++f) {
-      if (f == n_spec_st) {
-        if (spec_on) {
-          mbar_wait(&s_b2_done, n_spec_layers & 1);
-          ++n_spec_layers;
-          consumers_sync();
-        } else {
-          grid_sync(p.bar, P, tr ? tr + 212 : nullptr);
-        }
-        if (tr && tid == 0) tr[4] = globaltimer();
-        // ---------------- phase 3: compaction of my share ----------------
-        // One L2 round trip: all consumer threads stage the P counts, the union words and the
-        // per-token words (B > 1, or for the speculative corrections) into the ring slot the first
-        // cold FFN stage will use -- free now: every earlier stage has been consumed and the producer
-        // waits for ids_ready before reusing it.
-        const bool stage_tok = B > 1 || spec_on;
-        uint32_t *c_uni = reinterpret_cast<uint32_t *>(stage_ptr(it_ffn));   // [words]
-        uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (stage_tok)
-        int *c_cnt = reinterpret_cast<int *>(c_msk + (stage_tok ? B * p.words : 0));   // [P]
-        int *c_cntf = c_cnt + P;                                              // [P] (spec_on)
-        for (int i = tid; i < p.words; i += kConsumers) {
-          c_uni[i] = __ldcg(p.uni + i);
-          if (stage_tok)
-    #pragma unroll
-            for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
-        }
-        if (tid < P) {
-          c_cnt[tid] = __ldcg(p.counts + tid);
-          if (spec_on) c_cntf[tid] = __ldcg(p.counts_full + tid);
-        }
-        consumers_sync();
-        if (warp == 0) {
-          // CTA-block b owns words [b W/P, (b+1) W/P)
-          constexpr int KPL = 8;  // counts per lane (P <= 256)
-          int cv[KPL];
-    #pragma unroll
-          for (int i = 0; i < KPL; ++i) {
-            const int b = lane * KPL + i;
-            cv[i] = (b < P) ? c_cnt[b] : 0;
-          }
-          int lsum = 0;
-    #pragma unroll
-          for (int i = 0; i < KPL; ++i) lsum += cv[i];
-          int incl = lsum;
-    #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-          }
-          const int n = __shfl_sync(0xffffffffu, incl, 31);
-          const int k0 = (int)(((int64_t)c * n) / P), k1 = (int)(((int64_t)(c + 1) * n) / P);
-          if (k0 < k1) {
-            int pos = incl - lsum, cand = -1, cand_before = 0;
-    #pragma unroll
-            for (int i = 0; i < KPL; ++i) {
-              if (cand < 0 && pos + cv[i] > k0) {
-                cand = lane * KPL + i;
-                cand_before = pos;
-              }
-              pos += cv[i];
-            }
-            const uint32_t hit = __ballot_sync(0xffffffffu, cand >= 0);
-            const int src = __ffs(hit) - 1;
-            const int blk = __shfl_sync(0xffffffffu, cand, src);
-            int before = __shfl_sync(0xffffffffu, cand_before, src);
-            // walk union words from the start of block blk; keep ids with position in [k0, k1)
-            int w = (int)(((int64_t)blk * p.words) / P);
-            while (before < k1 && w < p.words) {
-              const int ww = w + lane;
-              const uint32_t u = (ww < p.words) ? c_uni[ww] : 0u;
-              uint32_t bitsb[B];
-    #pragma unroll
-              for (int b = 0; b < B; ++b) bitsb[b] = (B > 1 && ww < p.words) ? c_msk[b * p.words + ww] : u;
-              const int cnt = __popc(u);
-              int wincl = cnt;
-    #pragma unroll
-              for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, wincl, o);
-                if (lane >= o) wincl += t;
-              }
-              int my_pos = before + wincl - cnt;
-              uint32_t v = u;
-              while (v) {
-                const int bit = __ffs(v) - 1;
-                v &= v - 1;
-                if (my_pos >= k0 && my_pos < k1) {
-                  const int slot = my_pos - k0;
-                  s_ids[slot] = ww * 32 + bit;
-                  uint8_t tb = 0;
-    #pragma unroll
-                  for (int b = 0; b < B; ++b) tb |= (uint8_t)(((bitsb[b] >> bit) & 1u) << b);
-                  s_bits[slot] = tb;
-                }
-                ++my_pos;
-              }
-              before += __shfl_sync(0xffffffffu, wincl, 31);
-              w += 32;
-            }
-          }
-          int nfull = n;
-          if (spec_on) {   // the layer's union count includes the speculative neurons
-            int fs = 0;
-    #pragma unroll
-            for (int i = 0; i < KPL; ++i) fs += (lane * KPL + i < P) ? c_cntf[lane * KPL + i] : 0;
-            nfull = __reduce_add_sync(0xffffffffu, fs);
-          }
-          if (lane == 0) {
-            s_n = nfull;
-            s_k0 = k0;
-            s_k1 = k1;
-          }
-        } else if (warp == 1) {
-          // corrections: my speculative neurons whose bit is 0 for some token (ascending k, fixed order)
-          int nc = 0;
-          for (int k0 = 0; k0 < n_spec_c; k0 += 32) {
-            const int kk = k0 + lane;
-            bool need = false;
-            uint32_t tb = 0;
-            if (kk < n_spec_c) {
-              const int i = s_spec_ids[kk];
-    #pragma unroll
-              for (int b = 0; b < B; ++b) tb |= ((c_msk[b * p.words + (i >> 5)] >> (i & 31)) & 1u) << b;
-              need = tb != (1u << B) - 1u;
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, need);
-            if (need) {
-              const int slot = nc + __popc(bal & ((1u << lane) - 1u));
-              s_corr_ids[slot] = s_spec_ids[kk];
-    #pragma unroll
-              for (int b = 0; b < B; ++b) s_corr_h[slot][b] = ((tb >> b) & 1u) ? 0.f : -s_hspec[kk][b];
-            }
-            nc += __popc(bal);
-          }
-          if (lane == 0) s_ncorr = nc;
-        }
-        // generic-proxy writes to the scratch slot before the producer's TMA overwrites it
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        consumers_sync();
-        if (tid == 0) mbar_arrive(ids_ready);  // producer may stream this layer's FFN rows
-        if (tr && tid == 0) tr[5] = globaltimer();
-        {
-          const int k0 = s_k0;
-          n_mine = s_k1 - s_k0;
-          n_corr = s_ncorr;
-          for (int k = tid; k < n_mine; k += kConsumers) {
-            const int i = s_ids[k];
-            s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
-            if (p.ids_out) p.ids_out[k0 + k] = i;
-          }
-        }
-        if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
-        consumers_sync();
-
-        n_st = (n_mine + G - 1) / G;
-        n_corr_st = (n_corr + G - 1) / G;
-      }
-      if (f >= n_spec_st + n_st + n_corr_st) break;
-      const uint32_t it = it_spec + f;
-      const int fs = f - n_spec_st, fc = fs - n_st;   // index among the cold / correction stages
-      const int kk = (fs < 0 ? f : fc < 0 ? fs : fc) * G;
-      const int kn = min(G, (fs < 0 ? n_spec_c : fc < 0 ? n_mine : n_corr) - kk);
-      if (is_up) {
-        if (fs < 0) {
-          up_stage(it, kn, s_bspec + kk, nullptr, &s_hspec[kk]);
-        } else if (fc < 0) {
-          up_stage(it, kn, s_bup + kk, s_bits + kk, nullptr);
-        } else {
-          // h of a correction = minus the speculative h of each token whose bit is 0 (0 otherwise)
+      if constexpr (!SPEC) store_partial<B, CH>(yr, p.ypart + (size_t)c * B * d, d, gt, chunks);
+    }
+    int n_corr_st = 0;
+    if constexpr (SPEC) {
+      // corrections: a speculative neuron whose bit is 0 for token b gets h = -(its speculative h)
+      const int n_corr = s_ncorr;
+      n_corr_st = (n_corr + G - 1) / G;
+      for (int f = 0; f < n_corr_st; ++f) {
+        const uint32_t it = it_ffn + n_st + f;
+        const int kk = f * G, kn = min(G, n_corr - kk);
+        if (is_up) {
           wait_full(it);
           if (warp == 0) {
             if (lane < kn * B) hs[(it % NS) * (NA * B) + lane] = s_corr_h[kk + lane / B][lane % B];
             __syncwarp();
             if (lane == 0) mbar_arrive(&hready[it % NS]);
           }
+        } else {
+          wait_full(it);
+          mbar_wait(&hready[it % NS], (it / NS) & 1);
+          spec_down_stage<T, B, CH, NA>(pick<SPEC>(yrs, yrs), stage_ptr(it), hs + (it % NS) * (NA * B), kn, nb,
+                                        row_up, gt, chunks);
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cnt(&empty[it % NS], 2);  // 8 down warps x 2
         }
-      } else {
-        down_stage(it, kn);
       }
     }
-    if (!is_up) {
-      // partial y of this CTA -> global
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int ch = gt + q * kGroup;
-        if (ch < chunks) {
-#pragma unroll
-          for (int b = 0; b < B; ++b) {
-            float4 *dst = reinterpret_cast<float4 *>(p.ypart + ((size_t)c * B + b) * d + ch * 8);
-            __stcg(dst, make_float4(yr[q][0][b], yr[q][1][b], yr[q][2][b], yr[q][3][b]));
-            __stcg(dst + 1, make_float4(yr[q][4][b], yr[q][5][b], yr[q][6][b], yr[q][7][b]));
-          }
-        }
-      }
+    if constexpr (SPEC) {
+      if (!is_up) store_partial<B, CH>(yrs, p.ypart + (size_t)c * B * d, d, gt, chunks);
     }
     ring = it_ffn + n_st + n_corr_st;
 
@@ -1077,7 +1194,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 
 template <typename T, int B, bool REGLU, int CH, int NA>
 inline cudaError_t fused_launch_t(const FusedWork &w, const FusedParams &prm, cudaStream_t s) {
-  auto kern = k_layer<T, B, REGLU, CH, NA>;
+  auto kern = k_layer<T, B, REGLU, CH, NA, false>;
+  if constexpr (CH <= 4) {   // the speculative variant is instantiated for d <= 8192 only
+    if (prm.spec) kern = k_layer<T, B, REGLU, CH, NA, true>;
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, w.smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};

@@ -39,7 +39,7 @@
 
 namespace pi {
 
-constexpr int kGroupWarps = 7;                        // warps per group (up / down)
+constexpr int kGroupWarps = 8;                        // warps per group (up / down)
 constexpr int kGroup = kGroupWarps * 32;              // 256 threads per group
 constexpr int kConsumerWarps = 2 * kGroupWarps;       // 16
 constexpr int kConsumers = kConsumerWarps * 32;       // 512
@@ -79,6 +79,7 @@ struct FusedArgs {
   int32_t *ids_out, *n_out;
   const int32_t *hot_ids;
   int n_hot, hot_cap;
+  bool spec;   // stack launch whose layers carry speculative tables
 };
 
 struct LayerW {  // one layer's library-owned weights (device pointers)
@@ -288,7 +289,7 @@ inline cudaError_t fused_launch_stack(FusedWork &w, const FusedArgs &a, const La
   p.L = L;
   p.mask = w.mask;
   p.ids_out = nullptr;
-  p.spec = 1;   // layers without a speculative table (n_spec == 0) run unspeculated
+  p.spec = a.spec ? 1 : 0;   // the SPEC kernel variant; layers with n_spec == 0 run unspeculated in it
   return fused_launch_p<T>(w, p, a.reglu, a.B, s);
 }
 

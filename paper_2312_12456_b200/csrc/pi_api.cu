@@ -418,6 +418,7 @@ struct pi_stack {
   std::vector<pi_layer *> layers;
   LayerW *lws = nullptr;  // device [L]
   bool fused = false;
+  bool spec = false;      // some layer has a speculative hot prefix
 };
 
 extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, pi_stack **out) {
@@ -456,6 +457,7 @@ extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, 
     h[l].spec_ids = Ll->spec_ids;
     h[l].spec_words = Ll->spec_words;
     h[l].n_spec = Ll->n_spec;
+    if (Ll->n_spec > 0) S->spec = true;
   }
   if (cudaMalloc(&S->lws, sizeof(LayerW) * n_layers) != cudaSuccess) {
     delete S;
@@ -491,6 +493,7 @@ static pi_status stack_run_dev(pi_stack *S, const float *x, int B, float *y, int
       a.pred_relu = L0->pred_act == PI_PRED_RELU; a.reglu = L0->act == PI_ACT_REGLU;
       a.n_out = n_out;
       a.hot_cap = L0->hot_cap;
+      a.spec = S->spec;
       cudaError_t e = fused_launch_stack<T>(L0->fw, a, S->lws, n, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "stack: fused launch: %s", cudaGetErrorString(e));
       return PI_OK;
