@@ -58,9 +58,10 @@ def parse():
                          "neurons per layer whose profiled activation frequency is >= this, while the layer "
                          "synchronises after phase 2 (<= 0 disables; c4: 2.22 vs 2.30 ms/step)")
     ap.add_argument("--hot-cap", type=int, default=512, help="hot neurons prefetched per layer (pi_layer_desc.hot_cap)")
-    ap.add_argument("--spec-freq", type=float, default=0.99,
+    ap.add_argument("--spec-freq", type=float, default=0.0,
                     help="speculative hot prefix (pi_layer_desc.spec_freq): neurons with profiled frequency >= this "
-                         "are computed while the grid synchronises after the predictor (<= 0 disables)")
+                         "are computed while the grid synchronises after the predictor (<= 0: off, the default -- "
+                         "measured slower on c4, DESIGN.md)")
     ap.add_argument("--spec-cap", type=int, default=1 << 30, help="speculative neurons per layer (pi_layer_desc.spec_cap)")
     ap.add_argument("--l2-prefetch", type=int, default=0,
                     help="FFN stages L2-prefetched beyond the shared-memory ring (pi_layer_desc.l2_prefetch_stages)")
