@@ -63,8 +63,6 @@ def parse():
                          "are computed while the grid synchronises after the predictor (<= 0: off, the default -- "
                          "measured slower on c4, DESIGN.md)")
     ap.add_argument("--spec-cap", type=int, default=1 << 30, help="speculative neurons per layer (pi_layer_desc.spec_cap)")
-    ap.add_argument("--l2-prefetch", type=int, default=0,
-                    help="FFN stages L2-prefetched beyond the shared-memory ring (pi_layer_desc.l2_prefetch_stages)")
     ap.add_argument("--mean-act", type=float, default=0.10, help="mean activity of the planted profile (5-20%%)")
     ap.add_argument("--rank", dest="pred_rank", type=int, default=None, help="predictor rank r override")
     ap.add_argument("--no-phases", action="store_true", help="skip the traced per-phase breakdown pass")
@@ -430,8 +428,7 @@ def main():
         st, _ = build_stack(cfg, n_layers=n_layers, rank=rank, world=world, seed=args.seed + 1000 * c,
                             device=dev, max_batch=B, group=group, mean_act=args.mean_act, dims=layer_dims(args),
                             hot_freq=args.hot_freq if args.hot_freq > 0 else None, hot_cap=args.hot_cap, q4=args.q4,
-                            hot_caps=ilp_caps, spec_freq=args.spec_freq, spec_cap=args.spec_cap,
-                            l2_prefetch_stages=args.l2_prefetch)
+                            hot_caps=ilp_caps, spec_freq=args.spec_freq, spec_cap=args.spec_cap)
         stacks.append(st)
     d = cfg.d
     T = args.warmup + args.steps

@@ -128,10 +128,6 @@ typedef struct {
    * Speculative neurons are not L2-prefetched again by the hot-neuron prefetch. */
   float spec_freq;
   int32_t spec_cap;
-  /* Fused kernel: the producer also L2-prefetches the rows of the FFN stages this many stages
-   * beyond the shared-memory ring (a deeper pipeline without more shared memory); 0 = off.
-   * Moves no extra bytes (the prefetched rows are the ones the ring loads next). */
-  int32_t l2_prefetch_stages;
   pi_ffn_format ffn_format;  /* PI_FFN_16 (default, 0) or PI_FFN_Q4                         */
   const void *w_up_scale;    /* PI_FFN_Q4: dev fp16 [m_total, d/32]; else NULL               */
   const void *w_gate_scale;  /* PI_FFN_Q4 and REGLU: dev fp16 [m_total, d/32]; else NULL     */

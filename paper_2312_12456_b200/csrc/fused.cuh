@@ -629,22 +629,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       }
       mbar_wait(ids_ready, l & 1);                 // phase 3: after the ids are published
       const int n_mine = s_k1 - s_k0;
-      // L2 prefetch distance: while acquiring stage j also pull the rows of stage j + NS + l2pf - 1
-      // into L2 (the stages in between were prefetched by earlier iterations / the first pass)
-      const int pf = p.l2pf;
-      auto prefetch_stage = [&](int sj) {
-        const uint64_t keep = policy_evict_last();
-        for (int k = sj * G; k < min(n_mine, (sj + 1) * G); ++k) {
-          const int i = s_ids[k];
-          prefetch_l2(lw.w_up + (size_t)i * row_up, (uint32_t)row_up, keep);
-          prefetch_l2(lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, keep);
-        }
-      };
-      if (pf > 0)
-        for (int sj = NS; sj < NS + pf - 1; ++sj) prefetch_stage(sj);
       for (int k0 = 0; k0 < n_mine; k0 += G, ++it) {
         const int kn = min(G, n_mine - k0);
-        if (pf > 0) prefetch_stage(k0 / G + NS + pf - 1);
         uint8_t *dst = acquire((uint32_t)(kn * nb));
         const int s = it % NS;
         for (int k = 0; k < kn; ++k) {

@@ -80,7 +80,6 @@ struct FusedArgs {
   const int32_t *hot_ids;
   int n_hot, hot_cap;
   bool spec;   // stack launch whose layers carry speculative tables
-  int l2pf;    // FFN L2 prefetch distance beyond the ring, in stages
 };
 
 struct LayerW {  // one layer's library-owned weights (device pointers)
@@ -114,7 +113,6 @@ struct FusedParams {
   int kt;                     // 16-column K tiles of the fragment-major P2 (ceil(r / 16))
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int hot_cap;                // at most this many hot neurons are L2-prefetched per layer
-  int l2pf;                   // FFN stages L2-prefetched beyond the ring (0 = off)
 };
 
 // Everything below is host code (kernel launch parameters, workspace sizing, dispatch); the
@@ -260,7 +258,6 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.kt = w.kt;
   p.trace = w.trace;
   p.hot_cap = a.hot_cap;
-  p.l2pf = a.l2pf;
   return p;
 }
 

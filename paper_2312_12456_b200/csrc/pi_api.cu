@@ -88,7 +88,7 @@ struct pi_layer {
   unsigned *tickets_tc = nullptr;
   int S_tc = 0;
   int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons, hottest first
-  int n_hot = 0, hot_cap = 0, l2pf = 0;
+  int n_hot = 0, hot_cap = 0;
   int32_t *spec_ids = nullptr;             // [n_spec] speculative hot prefix, hottest first
   uint32_t *spec_words = nullptr;          // [words] bitmap of the speculative neurons
   int n_spec = 0;
@@ -296,7 +296,6 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
 
   cudaStream_t s = (cudaStream_t)stream;
   L->hot_cap = D->hot_cap > 0 ? D->hot_cap : PI_DEFAULT_HOT_CAP;
-  L->l2pf = std::max(0, std::min(64, D->l2_prefetch_stages));
   if (D->neuron_freq) {
     auto freq_of = [&](int k) { return D->neuron_freq[D->neuron_ids ? D->neuron_ids[k] : k]; };
     // speculative hot prefix: f >= spec_freq, hottest first (ties: ascending id), <= spec_cap
@@ -494,7 +493,6 @@ static pi_status stack_run_dev(pi_stack *S, const float *x, int B, float *y, int
       a.pred_relu = L0->pred_act == PI_PRED_RELU; a.reglu = L0->act == PI_ACT_REGLU;
       a.n_out = n_out;
       a.hot_cap = L0->hot_cap;
-      a.l2pf = L0->l2pf;
       a.spec = S->spec;
       cudaError_t e = fused_launch_stack<T>(L0->fw, a, S->lws, n, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "stack: fused launch: %s", cudaGetErrorString(e));
@@ -657,7 +655,7 @@ static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint3
       a.threshold = L->threshold; a.rmsnorm = (L->flags & PI_FLAG_INPUT_RMSNORM) != 0;
       a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
       a.mask_out = mask_out; a.ids_out = ids_out; a.n_out = n_out;
-      a.hot_ids = L->hot_ids; a.n_hot = L->n_hot; a.hot_cap = L->hot_cap; a.l2pf = L->l2pf;
+      a.hot_ids = L->hot_ids; a.n_hot = L->n_hot; a.hot_cap = L->hot_cap;
       cudaError_t e = fused_launch<T>(L->fw, a, L->num_sms, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "layer %d: fused launch: %s", L->layer_id, cudaGetErrorString(e));
       return PI_OK;

@@ -57,7 +57,7 @@ class LayerDesc(ctypes.Structure):
                 ("logit_threshold", ctypes.c_float), ("max_batch", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("neuron_freq", ctypes.POINTER(ctypes.c_float)),
                 ("hot_freq", ctypes.c_float), ("hot_cap", ctypes.c_int32), ("spec_freq", ctypes.c_float),
-                ("spec_cap", ctypes.c_int32), ("l2_prefetch_stages", ctypes.c_int32), ("ffn_format", ctypes.c_int),
+                ("spec_cap", ctypes.c_int32), ("ffn_format", ctypes.c_int),
                 ("w_up_scale", ctypes.c_void_p), ("w_gate_scale", ctypes.c_void_p),
                 ("w_down_scale", ctypes.c_void_p)]
 
@@ -146,8 +146,7 @@ class Layer:
     def __init__(self, w, neuron_ids: Optional[Sequence[int]] = None, max_batch: int = 1, flags: int = 0,
                  layer_id: int = 0, threshold: Optional[float] = None, pred_act: Optional[str] = None,
                  own_b_down: bool = True, stream=None, neuron_freq=None, hot_freq: float = 0.9,
-                 hot_cap: int = 0, q4=None, spec_freq: float = 0.0, spec_cap: int = 1 << 30,
-                 l2_prefetch_stages: int = 0):
+                 hot_cap: int = 0, q4=None, spec_freq: float = 0.0, spec_cap: int = 1 << 30):
         """w: gen.LayerWeights (16-bit global tensors).  q4: optional gen.Q4Weights -- the FFN
         then runs on INT4 neuron rows (PI_FFN_Q4); w still supplies the predictor and biases."""
         self.handle = None
@@ -181,7 +180,7 @@ class Layer:
                          *mats, _ptr(w.b_up),
                          _ptr(w.b_down) if own_b_down else None, _ptr(w.p_w1), _ptr(w.p_b1), _ptr(w.p_w2),
                          _ptr(w.p_b2), float(thr), int(max_batch), int(flags), freq_p, float(hot_freq),
-                         int(hot_cap), float(spec_freq), int(spec_cap), int(l2_prefetch_stages), *q4p)
+                         int(hot_cap), float(spec_freq), int(spec_cap), *q4p)
         h = ctypes.c_void_p()
         s = _stream(stream)
         _check(_lib.pi_layer_create(ctypes.byref(desc), s, ctypes.byref(h)))

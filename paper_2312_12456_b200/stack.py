@@ -121,7 +121,7 @@ def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, 
                 device="cuda", max_batch: int = 1, mean_act: float = 0.10, group=None,
                 keep_weights: bool = False, dims: Optional[dict] = None, hot_freq: Optional[float] = None,
                 hot_cap: int = 0, q4: bool = False, hot_caps: Optional[List[int]] = None,
-                spec_freq: float = 0.0, spec_cap: int = 1 << 30, l2_prefetch_stages: int = 0):
+                spec_freq: float = 0.0, spec_cap: int = 1 << 30):
     """Generate the config's layers (random init, seeded) and create this rank's handles.
 
     Returns (Stack, weights-or-None).  With keep_weights the generator tensors stay alive
@@ -141,7 +141,7 @@ def build_stack(cfg: gen.Config, n_layers: Optional[int] = None, rank: int = 0, 
         layers.append(pi.Layer(w, neuron_ids=nid, max_batch=max_batch, flags=flags, layer_id=l, own_b_down=own,
                                neuron_freq=freq, hot_freq=hot_freq if hot_freq is not None else 2.0,
                                hot_cap=hot_caps[l] if hot_caps is not None else hot_cap, q4=qw,
-                               spec_freq=spec_freq, spec_cap=spec_cap, l2_prefetch_stages=l2_prefetch_stages))
+                               spec_freq=spec_freq, spec_cap=spec_cap))
         del qw
         m_local = w.m if nid is None else len(nid)
         rowb = ((w.d // 2 + w.d // 16 + 15) // 16) * 16 if q4 else 2 * w.d
