@@ -324,7 +324,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
       // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping)
       const int jobs_here = 4 * (min(nwords, (st + 1) * wpp) - st * wpp);
       if (jj == 0) {
-        mbar_arrive(&x.hready[slot]);
+        mbar_arrive_cnt(&x.hready[slot], 32);
         mbar_arrive_cnt(&x.empty[slot], kConsumerWarps - jobs_here + 1);
       } else {
         mbar_arrive(&x.empty[slot]);
@@ -477,7 +477,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
-      mbar_init(&hready[s], 1);
+      mbar_init(&hready[s], 32);   // one warp's lanes (the h writers) per ring use
     }
     mbar_init(ids_ready, 1);
     mbar_init(p2_done, 1);
@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         float *rb = red + (st & 1) * kGroupWarps * kRedStride;
         up_partials<RPM * B>(acc, rb);
         if (gt == 0) {
-          mbar_arrive(&hready[it % NS]);                        // keep hready phases = ring uses
+          mbar_arrive_cnt(&hready[it % NS], 32);                // keep hready phases = ring uses
           mbar_arrive_cnt(&empty[it % NS], kConsumerWarps);     // every up warp has read the stage
         }
         if (gt < kn * B) {
@@ -851,7 +851,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
               if (hsave) hsave[g][b] = hv;
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&hready[it % NS]);
+            mbar_arrive(&hready[it % NS]);   // every writer lane releases its own h
           }
         };
         if (tid == 0) mbar_arrive(&s_b2_arrive);   // the agent lane arrives globally and polls
@@ -1079,7 +1079,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
             hs[(it % NS) * (NA * B) + lane] = ((s_bits[slot] >> b) & 1) ? hv : 0.f;
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&hready[it % NS]);
+          mbar_arrive(&hready[it % NS]);   // every writer lane releases its own h
         }
       }
     } else {
@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           if (warp == 0) {
             if (lane < kn * B) hs[(it % NS) * (NA * B) + lane] = s_corr_h[kk + lane / B][lane % B];
             __syncwarp();
-            if (lane == 0) mbar_arrive(&hready[it % NS]);
+            mbar_arrive(&hready[it % NS]);   // every writer lane releases its own h
           }
         } else {
           wait_full(it);
