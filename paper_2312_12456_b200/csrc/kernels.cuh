@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(256) k_predict2(const T *__restrict__ p2t, con
                                                    int words, uint32_t *__restrict__ mask,
                                                    float *__restrict__ logits, int nb) {
   constexpr int NT = (3 * B + 7) / 8;
-  constexpr int NC = NT >= 3 ? 1 : (NT == 2 ? 2 : 4);   // independent accumulator chains
+  constexpr int NC = NT >= 7 ? 1 : (NT >= 2 ? 2 : 4);   // independent accumulator chains
   extern __shared__ __align__(16) float p2smem[];
   const int ldg = kt * 16;
   float *gs = p2smem;                                          // [B][ldg]
@@ -500,12 +500,36 @@ cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float 
   return dispatch_batch(B, [&](auto bb) {
     constexpr int NB = decltype(bb)::value;
     const int g1 = (a.r + 1) / 2;
+    if constexpr (NB > 8) {
+      // B = 9..32: the hidden layer g = act_p(s P1 x + b1) is a real GEMM -- the batched
+      // tensor-core kernel with identity row ids and no mask (tc.cuh)
+      if (a.x3) {
+        k_split_x<T, NB><<<a.num_sms * 4, 256, 0, s>>>(x, B, a.d, a.x3);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        constexpr int N = 3 * NB;
+        const int st = 128 * kTcKB * 2 + N * 128;
+        const int smem = tc_stages(st) * st + 256;
+        e = cudaFuncSetAttribute(k_up_tc<T, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        k_up_tc<T, NB, false><<<std::min(a.num_sms, (a.r + 127) / 128 * 4), kTcThreads, smem, s>>>(
+            (const uint8_t *)a.p_w1, (const T *)a.p_b1, a.x3, scale, nullptr, nullptr, nullptr, 0, a.d, B, a.g, a.r,
+            nullptr, a.r, a.pred_relu);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        goto predict2;
+      }
+    }
     if (a.pred_relu)
       k_predict1<T, NB, true><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g, B);
     else
       k_predict1<T, NB, false><<<g1, 256, 0, s>>>((const T *)a.p_w1, (const T *)a.p_b1, x, scale, a.r, a.d, a.g, B);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    {
+      cudaError_t e0 = cudaGetLastError();
+      if (e0 != cudaSuccess) return e0;
+    }
+  predict2:
+    cudaError_t e = cudaSuccess;
     constexpr int NT = (3 * NB + 7) / 8;
     const size_t smem = (size_t)NB * a.kt * 16 * 4 + (size_t)a.kt * NT * 32 * 8 + (size_t)NB * 128 * 4;
     if (smem > 32 * 1024) {   // (the kernel's static shared memory counts against the 48 KB default too)
@@ -526,8 +550,9 @@ cudaError_t steps_ffn_tc(const StepArgs &a, const float *x, int B, const float *
   k_split_x<T, BMAX><<<a.num_sms * 4, 256, 0, s>>>(x, B, a.d, a.x3);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const int up_smem = kTcStages * ((a.reglu ? 2 : 1) * 128 * kTcKB * 2 + N * 128) + 256;
-  const int dn_smem = kTcStages * (128 * kTcKB * 2 + N * 128) + 256;
+  const int up_stage = (a.reglu ? 2 : 1) * 128 * kTcKB * 2 + N * 128, dn_stage = 128 * kTcKB * 2 + N * 128;
+  const int up_smem = tc_stages(up_stage) * up_stage + 256;
+  const int dn_smem = tc_stages(dn_stage) * dn_stage + 256;
   if (a.reglu) {
     e = cudaFuncSetAttribute(k_up_tc<T, BMAX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, up_smem);
     if (e != cudaSuccess) return e;

@@ -17,9 +17,11 @@ __global__ void __launch_bounds__(256) k_rms_scale(const float *__restrict__ x, 
   const int b = blockIdx.x;
   const float *xb = x + (int64_t)b * d;
   float s = 0.f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    const float v = xb[j];
-    s = fmaf(v, v, s);
+  // 16-byte loads, several in flight per thread (d % 8 == 0)
+#pragma unroll 4
+  for (int j = threadIdx.x * 4; j < d; j += blockDim.x * 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(xb + j));
+    s = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, s))));
   }
   __shared__ float red[8];
   s = warp_sum(s);

@@ -25,7 +25,12 @@
 namespace pi {
 
 constexpr int kTcKB = 64;        // K elements per stage (128 bytes of each 16-bit row)
-constexpr int kTcStages = 4;     // pipeline depth
+constexpr int kTcSmemBudget = 200 * 1024;   // pipeline shared memory per CTA
+constexpr int kTcMaxStages = 8;
+// pipeline depth for a stage of `stage_bytes`: as many stages as the budget holds (<= 8)
+__host__ __device__ constexpr int tc_stages(int stage_bytes) {
+  return kTcSmemBudget / stage_bytes < kTcMaxStages ? kTcSmemBudget / stage_bytes : kTcMaxStages;
+}
 constexpr int kTcThreads = 160;  // warps 0-3: producers + epilogue (TMEM lanes 0-127), warp 4: MMA issue
 
 __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
@@ -91,14 +96,14 @@ __global__ void k_split_x(const float *__restrict__ x, int nb, int d, uint16_t *
   }
 }
 
-template <int kLag>
+template <int kLag, int kStages>
 struct TcArrive {   // producer-side bookkeeping: arrive on full[] once a stage's cp.async copies landed
   uint32_t it = 0, arrived = 0;
   __device__ __forceinline__ void after_issue(uint64_t *full) {
     cp_async_wait<kLag>();
     fence_proxy_async_smem();
     while ((int)arrived <= (int)it - kLag) {
-      tc_mbar_arrive(&full[arrived % kTcStages]);
+      tc_mbar_arrive(&full[arrived % kStages]);
       ++arrived;
     }
     ++it;
@@ -107,7 +112,7 @@ struct TcArrive {   // producer-side bookkeeping: arrive on full[] once a stage'
     cp_async_wait<0>();
     fence_proxy_async_smem();
     while (arrived < it) {
-      tc_mbar_arrive(&full[arrived % kTcStages]);
+      tc_mbar_arrive(&full[arrived % kStages]);
       ++arrived;
     }
   }
@@ -122,18 +127,21 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" :::
 // own mask bit, writes h [nb, hstride] and the down GEMM's B operand h3 (tc_b_offset over
 // positions; positions [n, 64 ceil(n / 64)) zero).
 // ---------------------------------------------------------------------------
+// Also the predictor's hidden layer (a1) for B = 9..32: ids = NULL (row k = position k, n = the
+// row count), mask = NULL (no per-token bits), relu = the act_p choice, h3 = NULL.
 template <typename T, int BMAX, bool REGLU>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_up_tc(const uint8_t *__restrict__ wup, const T *__restrict__ bup, const uint16_t *__restrict__ x3,
             const float *__restrict__ scale, const int32_t *__restrict__ ids, const int32_t *__restrict__ n_active,
             const uint32_t *__restrict__ mask, int words, int d, int nb, float *__restrict__ h, int hstride,
-            uint16_t *__restrict__ h3) {
+            uint16_t *__restrict__ h3, int n_rows = 0, bool relu = true) {
   constexpr int N = 3 * BMAX;
   constexpr int NPL = REGLU ? 2 : 1;         // plane 0: up, plane 1: gate
   constexpr int A_BYTES = 128 * kTcKB * 2;   // 16 KB per plane
   constexpr int B_BYTES = N * 128;
   constexpr int STAGE = NPL * A_BYTES + B_BYTES;
-  constexpr int kLag = 2;
+  constexpr int kTcStages = tc_stages(STAGE);
+  constexpr int kLag = kTcStages - 2;   // cp.async groups kept in flight per producer thread
   extern __shared__ __align__(128) uint8_t tsm[];
   uint64_t *full = reinterpret_cast<uint64_t *>(tsm + kTcStages * STAGE);
   uint64_t *empty = full + kTcStages;
@@ -141,7 +149,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t *acc_empty = acc_full + 2;       // [2]
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int n = *n_active;
+  const int n = ids ? *n_active : n_rows;
   const int G = gridDim.x;
   const int Tn = max(G, (n + 127) / 128);
   const int KB = d / kTcKB;
@@ -194,12 +202,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ---------------- producers, then the epilogue of each chunk (thread = TMEM lane = row) ----------------
-    TcArrive<kLag> arr;
+    TcArrive<kLag, kTcStages> arr;
     const int row = tid;
     int ci = 0;
     for (int t = blockIdx.x; t < Tn; t += G, ++ci) {
       const int p0 = (int)(((int64_t)t * n) / Tn), p1 = (int)(((int64_t)(t + 1) * n) / Tn), R = p1 - p0;
-      const int i = row < R ? ids[p0 + row] : 0;
+      const int i = row < R ? (ids ? ids[p0 + row] : p0 + row) : 0;
       const uint8_t *src = wup + (int64_t)i * rowb;
       for (int kb = 0; kb < KB; ++kb) {
         const uint32_t it = arr.it;
@@ -255,14 +263,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (b < nb) {
               const float s_b = scale ? scale[b] : 1.f;
               const float a = ((vu[3 * bb] + vu[3 * bb + 1]) + vu[3 * bb + 2]) * s_b + bu;
-              hv = REGLU ? fmaxf(((vg[3 * bb] + vg[3 * bb + 1]) + vg[3 * bb + 2]) * s_b, 0.f) * a : fmaxf(a, 0.f);
-              if (!((mask[(int64_t)b * words + (i >> 5)] >> (i & 31)) & 1u)) hv = 0.f;
+              hv = REGLU ? fmaxf(((vg[3 * bb] + vg[3 * bb + 1]) + vg[3 * bb + 2]) * s_b, 0.f) * a
+                         : (relu ? fmaxf(a, 0.f) : a);
+              if (mask && !((mask[(int64_t)b * words + (i >> 5)] >> (i & 31)) & 1u)) hv = 0.f;
               h[(int64_t)b * hstride + pos] = hv;
             }
-            uint16_t p[3];
-            Split3<T>::split(hv, p);
+            if (h3) {
+              uint16_t p[3];
+              Split3<T>::split(hv, p);
 #pragma unroll
-            for (int s = 0; s < 3; ++s) h3[tc_b_offset(3 * b + s, pos, N) / 2] = p[s];
+              for (int s = 0; s < 3; ++s) h3[tc_b_offset(3 * b + s, pos, N) / 2] = p[s];
+            }
           }
         }
       }
@@ -270,7 +281,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_mbar_arrive(&acc_empty[ab]);
     }
     // positions [n, 64 ceil(n / 64)) of the down GEMM's B operand are zero
-    if (blockIdx.x == 0) {
+    if (h3 && blockIdx.x == 0) {
       const int pend = (n + kTcKB - 1) / kTcKB * kTcKB;
       for (int e = tid; e < (pend - n) * N; e += 128) h3[tc_b_offset(e % N, n + e / N, N) / 2] = 0;
     }
@@ -296,7 +307,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   constexpr int A_BYTES = 128 * kTcKB * 2;   // 128 columns x 64 neurons
   constexpr int B_BYTES = N * 128;
   constexpr int STAGE = A_BYTES + B_BYTES;
-  constexpr int kLag = 2;
+  constexpr int kTcStages = tc_stages(STAGE);
+  constexpr int kLag = kTcStages - 2;
   extern __shared__ __align__(128) uint8_t tsm[];
   uint64_t *full = reinterpret_cast<uint64_t *>(tsm + kTcStages * STAGE);
   uint64_t *empty = full + kTcStages;
@@ -354,7 +366,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {
-    TcArrive<kLag> arr;
+    TcArrive<kLag, kTcStages> arr;
     int ci = 0;
     const int kr = tid >> 1, half = tid & 1;   // neuron (row of the K block) and which 8 of its 16 chunks
     for (int item = blockIdx.x; item < items; item += gridDim.x, ++ci) {

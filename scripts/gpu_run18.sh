@@ -1,0 +1,6 @@
+python paper_2312_12456_b200/build.py > /dev/null
+timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitizer_racecheck.txt 2>&1; echo "racecheck $(grep -E 'RACECHECK SUMMARY' gpurun_out/sanitizer_racecheck.txt | tail -1)"
+timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitizer_synccheck.txt 2>&1; echo "synccheck $(grep -E 'ERROR SUMMARY' gpurun_out/sanitizer_synccheck.txt | tail -1)"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' --csv --log-file gpurun_out/launches_c3b16.csv python bench.py --config c3 --batch 16 --layers 4 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-phases > gpurun_out/ncu_c3b16.log 2>&1; echo ncu=$?
+python scripts/ncu_summary.py launches gpurun_out/launches_c3b16.csv 2>&1 | head -30
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "integer or golden or stack" 2>&1 | tail -2
