@@ -190,6 +190,13 @@ __device__ __forceinline__ void tile_logits(const float (&c)[NT][4], int b, floa
   }
 }
 
+// INT4 neuron rows (PI_FFN_Q4, reading R21): element k of a 32-bit code word is nibble k (byte b:
+// element 2b low, 2b + 1 high); (2^23 + q) - (2^23 + 8) = q - 8 exactly
+__device__ __forceinline__ void q4_unpack8(uint32_t v, float (&f)[8]) {
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = __int_as_float(0x4B000000 | ((v >> (4 * e)) & 15u)) - 8388616.0f;
+}
+
 // Load 8 consecutive fp32 activations (32-B aligned chunk) through the cached path.
 __device__ __forceinline__ void ld_x8(const float *p, float (&f)[8]) {
   const float4 a = __ldg(reinterpret_cast<const float4 *>(p));

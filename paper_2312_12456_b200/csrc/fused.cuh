@@ -83,6 +83,10 @@ __device__ __forceinline__ Pack8 lds128z(const uint8_t *base, size_t off, bool o
   for (int k = 0; k < 4; ++k) w.u[k] = ok ? w.u[k] : 0u;
   return w;
 }
+__device__ __forceinline__ uint32_t lds32(const uint8_t *p) { return *reinterpret_cast<const uint32_t *>(p); }
+__device__ __forceinline__ float lds_half(const uint8_t *p) {
+  return __half2float(__ushort_as_half(*reinterpret_cast<const unsigned short *>(p)));
+}
 __device__ __forceinline__ void consumers_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
@@ -416,7 +420,9 @@ __device__ __forceinline__ void spec_down_stage(float (&yr)[CH][8][B], const uin
 // SPEC variant: see k_layer below
 // SPEC: the speculative hot prefix (pi_layer_desc.spec_freq) -- a separate instantiation, so the
 // default kernel carries none of its code (it costs registers: measured slower).
-template <typename T, int B, bool REGLU, int CH, int NA, bool SPEC>
+// Q4: the FFN rows are INT4 records (PI_FFN_Q4, row f3; B = 1): a thread's 8-element chunk of d is
+// one 32-bit word of codes and one fp16 scale, dequantised in registers (w = s (q - 8)).
+template <typename T, int B, bool REGLU, int CH, int NA, bool SPEC, bool Q4>
 __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p) {
   constexpr int RPM = (NA == 1) ? 2 : 8;      // max P1 rows per stage
   extern __shared__ __align__(128) uint8_t fsmem[];
@@ -468,8 +474,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   // P2 stages that fit the ring at the layer start (the rest stream in as slots recycle; their
   // rows are L2-prefetched during the previous layer's tail)
   const int st_p2_ring = min(st_p2, max(0, NS - st_p1));
-  const size_t row_up = (size_t)d * 2 * (REGLU ? 2 : 1);  // bytes of one up (gate|up) row
-  const size_t row_dn = (size_t)d * 2;
+  // FFN rows: 16-bit (d * 2 bytes) or INT4 records (Q4: d/2 code bytes + d/32 fp16 scales, padded)
+  const size_t row_ffn = Q4 ? (size_t)p.rec_q4 : (size_t)d * 2;
+  const size_t row_up = row_ffn * (REGLU ? 2 : 1);         // bytes of one up (gate|up) row
+  const size_t row_dn = row_ffn;
+  const size_t row_p1 = (size_t)d * 2;                     // predictor rows stay 16-bit
   const size_t nb = row_up + row_dn;                       // bytes per neuron in a stage
   auto layer = [&](int l) -> LayerW { return p.lws ? p.lws[l] : p.lw0; };
 
@@ -557,7 +566,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
         for (int st = NS; st < st_p1; ++st) {
           const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
           for (int k = 0; k < kn; ++k)
-            prefetch_l2(lw.p_w1 + (size_t)(c + (k0 + k) * P) * row_dn, (uint32_t)row_dn, keep);
+            prefetch_l2(lw.p_w1 + (size_t)(c + (k0 + k) * P) * row_p1, (uint32_t)row_p1, keep);
         }
         if (st_p2_ring < st_p2) {
           const size_t a0 = (size_t)(w0 + st_p2_ring * p.words_p2) * 32 * rowb2, a1 = (size_t)w1 * 32 * rowb2;
@@ -579,11 +588,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       for (int st = 0; st < st_p1; ++st, ++it) {  // phase 1: P1 rows c, c+P, ...
         prefetch_tail(st);
         const int k0 = st * RP1, kn = min(RP1, n_p1 - k0);
-        uint8_t *dst = acquire((uint32_t)(kn * row_dn));
+        uint8_t *dst = acquire((uint32_t)(kn * row_p1));
         const int s = it % NS;
         for (int k = 0; k < kn; ++k) {
           const int j = c + (k0 + k) * P;
-          bulk_g2s(dst + (size_t)k * row_dn, lw.p_w1 + (size_t)j * row_dn, (uint32_t)row_dn, &full[s], pol);
+          bulk_g2s(dst + (size_t)k * row_p1, lw.p_w1 + (size_t)j * row_p1, (uint32_t)row_p1, &full[s], pol);
         }
       }
       for (int st = 0; st < st_p2; ++st, ++it) {  // phase 2: P2 words [w0, w1), contiguous
@@ -758,7 +767,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
           for (int q = 0; q < CH; ++q) {
             const int ch = gt + q * kGroup;
             float wf[8];
-            WT<T>::unpack(lds128z(buf, (size_t)k * row_dn + (size_t)ch * 16, k < kn && ch < chunks), wf);
+            WT<T>::unpack(lds128z(buf, (size_t)k * row_p1 + (size_t)ch * 16, k < kn && ch < chunks), wf);
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
@@ -1042,6 +1051,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 #pragma unroll
         for (int g = 0; g < NA; ++g) {
           const size_t go = (size_t)g * nb;
+          if constexpr (Q4) {
+            // INT4 records: [gate record |] up record; per chunk a code word and its group scale
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const int ch = gt + q * kGroup;
+              const bool ok = g < kn && ch < chunks;
+              const size_t cu = go + (REGLU ? row_ffn : 0);
+              float fu[8], pu = 0.f;
+              q4_unpack8(ok ? lds32(buf + cu + (size_t)ch * 4) : 0x88888888u, fu);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) pu = fmaf(fu[e], xr[q][e][0], pu);
+              const float su = ok ? lds_half(buf + cu + (size_t)(d >> 1) + (size_t)(ch >> 2) * 2) : 0.f;
+              const int ai = REGLU ? g * 2 : g;
+              acc[ai] = fmaf(su, pu, acc[ai]);
+              if (REGLU) {
+                float fg[8], pg = 0.f;
+                q4_unpack8(ok ? lds32(buf + go + (size_t)ch * 4) : 0x88888888u, fg);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) pg = fmaf(fg[e], xr[q][e][0], pg);
+                const float sg = ok ? lds_half(buf + go + (size_t)(d >> 1) + (size_t)(ch >> 2) * 2) : 0.f;
+                acc[g * 2 + 1] = fmaf(sg, pg, acc[g * 2 + 1]);
+              }
+            }
+            continue;
+          }
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
             const int ch = gt + q * kGroup;
@@ -1106,6 +1140,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 #pragma unroll
           for (int b = 0; b < B; ++b) h[b] = (g < kn) ? hh[g * B + b] : 0.f;
           const size_t go = (size_t)g * nb + row_up;
+          if constexpr (Q4) {
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+              const int ch = gt + q * kGroup;
+              const bool ok = g < kn && ch < chunks;
+              float wf[8];
+              q4_unpack8(ok ? lds32(buf + go + (size_t)ch * 4) : 0x88888888u, wf);
+              const float hs_ = ok ? h[0] * lds_half(buf + go + (size_t)(d >> 1) + (size_t)(ch >> 2) * 2) : 0.f;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) yr[q][e][0] = fmaf(hs_, wf[e], yr[q][e][0]);
+            }
+            continue;
+          }
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
             const int ch = gt + q * kGroup;
@@ -1194,9 +1241,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 
 template <typename T, int B, bool REGLU, int CH, int NA>
 inline cudaError_t fused_launch_t(const FusedWork &w, const FusedParams &prm, cudaStream_t s) {
-  auto kern = k_layer<T, B, REGLU, CH, NA, false>;
+  auto kern = k_layer<T, B, REGLU, CH, NA, false, false>;
   if constexpr (CH <= 4) {   // the speculative variant is instantiated for d <= 8192 only
-    if (prm.spec) kern = k_layer<T, B, REGLU, CH, NA, true>;
+    if (prm.spec) kern = k_layer<T, B, REGLU, CH, NA, true, false>;
+  }
+  if constexpr (B == 1) {    // INT4 rows (the speculative variant is 16-bit only)
+    if (prm.rec_q4 > 0) kern = k_layer<T, B, REGLU, CH, NA, false, true>;
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, w.smem);
   if (e != cudaSuccess) return e;
@@ -1221,6 +1271,7 @@ cudaError_t fused_launch_tbr(const FusedWork &w, const FusedParams &p, int CH, i
   PI_FL(1, 8) PI_FL(1, 1) PI_FL(2, 8) PI_FL(2, 1) PI_FL(3, 1) PI_FL(4, 1)
   if constexpr (B == 1) {   // wider d keeps x and y register-resident only for one token
     PI_FL(5, 1) PI_FL(6, 1) PI_FL(7, 1) PI_FL(8, 1)
+    PI_FL(3, 4) PI_FL(4, 4) PI_FL(6, 4)   // INT4 rows, 2-4 neurons per stage
   }
 #undef PI_FL
   return cudaErrorNotSupported;

@@ -60,6 +60,7 @@ struct FusedWork {
   unsigned long long *bar = nullptr;  // grid barrier counter (monotonic)
   float *g = nullptr;                 // [maxB, r]
   float *ypart = nullptr;             // [P, maxB, d]
+  int rec_q4 = 0;                     // INT4 FFN records: bytes per neuron and matrix (0 = 16-bit rows)
   int *counts = nullptr;              // [P]
   int *counts_full = nullptr;         // [P]
   uint32_t *mask = nullptr;           // [maxB, words]
@@ -111,6 +112,7 @@ struct FusedParams {
   int spec;                   // speculative hot prefix on (stack launches only)
   int NS, stage_bytes, G, rows_p1, words_p2, idcap, wcap, part_off, pcap;
   int kt;                     // 16-column K tiles of the fragment-major P2 (ceil(r / 16))
+  int rec_q4;                 // INT4 FFN records (bytes per neuron and matrix); 0 = 16-bit rows
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int hot_cap;                // at most this many hot neurons are L2-prefetched per layer
 };
@@ -123,8 +125,10 @@ struct FusedParams {
 inline int fused_ch(int d) { return (d / 8 + kGroup - 1) / kGroup; }
 
 template <class Alloc>
-inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc) {
+inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc,
+                        int rec_q4 = 0) {
   w = FusedWork{};
+  w.rec_q4 = rec_q4;
   w.d = d;
   w.m = m;
   w.r = r;
@@ -136,7 +140,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.kt = (r + 15) / 16;
   const size_t p2_word = (size_t)32 * w.kt * 16 * 2;   // one 32-row word of the tiled P2
   // stage: >= one neuron (gate|up + down), one P2 word, >= 32 KB
-  const size_t nb = (size_t)d * (reglu ? 6 : 4);
+  const size_t nb = rec_q4 ? (size_t)rec_q4 * (reglu ? 3 : 2) : (size_t)d * (reglu ? 6 : 4);
   size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, p2_word});
   sb = (sb + 127) / 128 * 128;
   // compaction stages the union words, the per-token words and the P counts in one ring slot
@@ -184,9 +188,10 @@ inline void fused_init(FusedWork &w, cudaStream_t s) {
 
 // neurons per stage (NA template bound and runtime G) and P1 rows per stage
 inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *NA, int *G, int *RP1) {
-  const size_t nb = (size_t)d * 2 * (reglu ? 3 : 2);
+  const size_t nb = w.rec_q4 ? (size_t)w.rec_q4 * (reglu ? 3 : 2) : (size_t)d * 2 * (reglu ? 3 : 2);
   const int g = (int)(w.stage_bytes / nb);
-  *NA = g >= 2 ? 8 : 1;
+  // 8 neurons per stage when they fit; INT4 rows of wide layers (2-4 per stage) use the 4 variant
+  *NA = g >= 2 ? ((w.rec_q4 && g <= 4) ? 4 : 8) : 1;
   *G = std::min(*NA, std::max(1, g));
   const int rp = (int)(w.stage_bytes / ((size_t)d * 2));
   *RP1 = std::max(1, std::min(*NA == 1 ? 2 : 8, rp));
@@ -194,11 +199,13 @@ inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *NA, int *
 
 inline bool fused_supported(const FusedWork &w, int B = 1) {
   if (!w.enabled || B < 1 || B > kFusedMaxB) return false;
+  if (w.rec_q4 && B != 1) return false;   // INT4 rows: the fused kernel is instantiated for B = 1
   const int ch = fused_ch(w.d);
   if (ch * 8 * B > 64) return false;  // register-resident x / y per group thread
   int NA, G, RP1;
   fused_geometry(w, w.d, w.reglu, &NA, &G, &RP1);
   // the instantiated (CH, NA) combinations (fused_launch_tbr)
+  if (NA == 4) return B == 1 && (ch == 3 || ch == 4 || ch == 6);
   if (ch <= 2) return true;
   return NA == 1 && (ch <= 4 || (B == 1 && ch <= kMaxCH));
 }
@@ -256,6 +263,7 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.part_off = w.part_off;
   p.pcap = w.pcap;
   p.kt = w.kt;
+  p.rec_q4 = w.rec_q4;
   p.trace = w.trace;
   p.hot_cap = a.hot_cap;
   return p;

@@ -317,11 +317,6 @@ __global__ void __launch_bounds__(256) k_down(const T *__restrict__ wdt, const T
 // layout: one record per neuron (and per matrix) = d/2 code bytes then d/32 fp16 scales, padded
 // to 16 bytes; ReGLU up records are [gate record | up record].  w = s_g * (q - 8).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void q4_unpack8(uint32_t v, float (&f)[8]) {
-  // element k of the word = nibble k (byte b: element 2b low, 2b + 1 high); (2^23 + q) - (2^23 + 8)
-#pragma unroll
-  for (int e = 0; e < 8; ++e) f[e] = __int_as_float(0x4B000000 | ((v >> (4 * e)) & 15u)) - 8388616.0f;
-}
 
 // a4 over INT4 rows: one warp per active neuron; lane walks 32-element groups (16 code bytes +
 // one fp16 scale per matrix); per group the integer-code dot product is scaled once.
@@ -512,7 +507,7 @@ cudaError_t steps_predict(const StepArgs &a, const float *x, int B, const float 
         const int smem = tc_stages(st) * st + 256;
         e = cudaFuncSetAttribute(k_up_tc<T, NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        k_up_tc<T, NB, false><<<std::min(a.num_sms, (a.r + 127) / 128 * 4), kTcThreads, smem, s>>>(
+        k_up_tc<T, NB, false><<<a.num_sms, kTcThreads, smem, s>>>(
             (const uint8_t *)a.p_w1, (const T *)a.p_b1, a.x3, scale, nullptr, nullptr, nullptr, 0, a.d, B, a.g, a.r,
             nullptr, a.r, a.pred_relu);
         e = cudaGetLastError();

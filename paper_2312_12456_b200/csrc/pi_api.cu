@@ -287,10 +287,10 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
     ALLOC(L->partial_tc, (size_t)L->S_tc * bmax * d * 4, false);
     ALLOC(L->tickets_tc, (size_t)(d / 128) * 4, false);
   }
-  // the fused kernel streams 16-bit rows; INT4 layers run the per-step kernels
-  if (!q4 && !fused_alloc(L->fw, d, ml, r, MB, L->num_sms, reglu, [&](void **p, size_t bytes) {
+  // the fused kernel streams 16-bit rows or INT4 records (B = 1)
+  if (!fused_alloc(L->fw, d, ml, r, MB, L->num_sms, reglu, [&](void **p, size_t bytes) {
         return dev_alloc(L, p, bytes, false) == PI_OK;
-      }))
+      }, q4 ? (int)L->rec_q4 : 0))
     return cleanup(fail(PI_ERR_OUT_OF_MEMORY, "layer %d: fused workspace", lid));
 #undef ALLOC
 
