@@ -28,10 +28,11 @@ def main():
     ap.add_argument("--stack", action="store_true", help="trace layer 1 of a pi_stack_run launch")
     ap.add_argument("--hot-freq", type=float, default=0.0, help="hot-neuron L2 prefetch threshold (0 = off)")
     ap.add_argument("--spec-freq", type=float, default=0.0, help="speculative hot prefix threshold (0 = off)")
+    ap.add_argument("--q4", action="store_true", help="INT4 FFN rows")
     a = ap.parse_args()
     cfg = gen.CONFIGS[a.config]
     st, _ = build_stack(cfg, n_layers=min(a.layers, cfg.layers), device="cuda", max_batch=a.batch,
-                        hot_freq=a.hot_freq if a.hot_freq > 0 else None, spec_freq=a.spec_freq)
+                        hot_freq=a.hot_freq if a.hot_freq > 0 else None, spec_freq=a.spec_freq, q4=a.q4)
     P = st.layers[0].info.num_sms
     buf = torch.zeros(P * 256, dtype=torch.int64, device="cuda")
     x = gen.tokens(a.batch, cfg.d, seed=3, device="cuda")
