@@ -24,7 +24,7 @@ def launches(path):
             continue
         v = float(r[mv].replace(",", ""))
         unit = r[mu]
-        us = v / 1e3 if unit == "nsecond" else (v if unit == "usecond" else v * 1e3 if unit == "msecond" else v)
+        us = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0) * v
         name = r[k].split("(")[0][:90]
         agg[name].append(us)
     tot = sum(sum(v) for v in agg.values())
