@@ -14,7 +14,9 @@ down [-> NCCL all-reduce for N > 1]).  Default workload: configs[3] of BASELINE.
 Falcon-40B-ReLU FFN stack (d 8192, m 32768, 60 layers, predictor rank 512), the config the
 metric's "1/2/4/8 B200" refers to; it fits one GPU (64 GB of FFN weights), so at N = 1 it is
 the single-GPU workload and at N > 1 it is neuron-sharded across ranks (strong scaling).
-``--config c2`` runs the single OPT-6.7B layer (rotated over 16 copies to defeat L2).
+``--config c1`` / ``c2`` (single layers) run the grouped launch (pi_group_run): the SMs split into
+independent groups, each decoding its own token through its own chain of layer copies (distinct
+seeded weights, so every step streams far more than L2); value = layer-tokens per second.
 
 Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
 """
@@ -47,7 +49,14 @@ def parse():
     ap.add_argument("--config", default="c4")
     ap.add_argument("--batch", type=int, default=None)
     ap.add_argument("--layers", type=int, default=None, help="override the layer count (debug only)")
-    ap.add_argument("--copies", type=int, default=16, help="layer copies rotated for single-layer configs")
+    ap.add_argument("--copies", type=int, default=16, help="layer copies rotated for single-layer configs (--no-group)")
+    ap.add_argument("--group-ctas", type=int, default=0,
+                    help="single-layer configs: CTAs per independent problem of the grouped launch (pi_group_run); "
+                         "0 = the config default (c1: 2, c2: 8)")
+    ap.add_argument("--group-layers", type=int, default=4, help="layer copies chained per group (grouped launch)")
+    ap.add_argument("--no-group", action="store_true",
+                    help="single-layer configs: one pi_layer_forward per step over rotated copies instead of the "
+                         "grouped launch")
     ap.add_argument("--impl", default="pi", choices=["pi", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -377,6 +386,104 @@ def dry_run(args, cfg, B, n_layers):
         dist.destroy_process_group()
 
 
+GROUP_CTAS_DEFAULT = {"c1": 2, "c2": 8}
+
+
+def run_grouped(args, cfg, B, dev):
+    """Single-layer configs (c1, c2): NG independent problems of group_ctas CTAs each in ONE
+    persistent launch (pi_group_run); group k chains --group-layers distinct copies of the layer.
+    One step = one launch = every group's token through its layer copies."""
+    from paper_2312_12456_b200 import gen, pi
+    from paper_2312_12456_b200.stack import algorithmic_bytes, build_stack
+
+    pg = args.group_ctas or GROUP_CTAS_DEFAULT.get(cfg.name, 8)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    ng, gl = n_sm // pg, args.group_layers
+    stacks = []
+    for k in range(ng):
+        # no hot-neuron L2 prefetch: every group would pull its own hot rows into the shared L2
+        st, _ = build_stack(cfg, n_layers=gl, seed=args.seed + 1000 * k, device=dev, max_batch=1,
+                            mean_act=args.mean_act, dims=layer_dims(args))
+        if st.stack is not None:
+            st.stack.close()          # the group owns the launch
+            st.stack = None
+        stacks.append(st)
+    G = pi.GroupHandle([st.layers for st in stacks], pg)
+    d = cfg.d
+    T = args.warmup + args.steps
+    xs = torch.stack([torch.cat([gen.tokens(1, d, seed=args.seed + 7 + 31 * k, step=i, device=dev)[None]
+                                 for k in range(ng)]) for i in range(T)])          # [T, NG, 1, d]
+    y = torch.empty(ng, 1, d, device=dev)
+    nbuf = torch.zeros(T, ng, gl, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+    for i in range(args.warmup):
+        G.run(xs[i], y, nbuf[i])
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index or 0)
+    clocks.start()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for k in range(args.steps):
+        G.run(xs[args.warmup + k], y, nbuf[args.warmup + k])
+        evs[k + 1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    per_step = np.array([evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)])
+    total_ms = evs[0].elapsed_time(evs[-1])
+    ms_per_step = total_ms / args.steps
+    lt = ng * gl * B                                         # layer-tokens per step
+    value = lt * args.steps / (total_ms / 1e3)
+    n_host = nbuf.cpu().numpy()[args.warmup:]
+    meta = stacks[0].metas[0]
+    bytes_step = np.array([sum(algorithmic_bytes(meta, int(v), B) for v in n_host[k].ravel())
+                           for k in range(args.steps)])
+    realised = float(n_host.mean() / meta.m_local)
+    peak, peak_src = hbm_peak()
+    launch_s = per_step / 1e3
+    achieved = float(bytes_step.mean()) / float(launch_s.mean()) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_layer grouped launch (pi_group_run): %d groups x %d CTAs, %d layer "
+                "copies per group" % (ng, pg, gl), "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "traffic_source": None, "peak_source": peak_src,
+                "bytes_per_launch": int(bytes_step.mean()), "launch_us": round(float(launch_s.mean()) * 1e6, 2),
+                "timing": "CUDA events around each launch inside the timed loop",
+                "step_frac": round(float(bytes_step.mean()) / (ms_per_step / 1e3) / 1e9 / peak, 4)}
+    e2e = None
+    if not args.no_e2e:
+        xh = xs.cpu().pin_memory()
+        yh = torch.empty(ng, 1, d).pin_memory()
+        xd = torch.empty(ng, 1, d, device=dev)
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            xd.copy_(xh[args.warmup + k], non_blocking=True)
+            G.run(xd, y)
+            yh.copy_(y, non_blocking=True)
+            stream.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": lt * args.steps / e2e_s, "unit": "tokens/s", "h2d_bytes_per_step": ng * B * d * 4,
+               "d2h_bytes_per_step": ng * B * d * 4,
+               "api": "pinned host copy + pi_group_run + host copy (GroupHandle.run)"}
+    args.hot_freq = 0.0      # reported in config: off for grouped launches
+    cpu = None if args.no_cpu_baseline else oracle_baseline(cfg, args.seed, 1, B, args.ref_seconds, dev,
+                                                             layer_dims(args))
+    out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+           "config": workload_config(cfg, B, 1, 1, {
+               "realised_activity": round(realised, 4),
+               "grouped": {"groups": ng, "ctas_per_group": pg, "layer_copies_per_group": gl,
+                           "layer_tokens_per_step": lt,
+                           "note": "value = layer-tokens/s: each group decodes its own token through its own "
+                                   "chain of distinct layer copies; all groups in one persistent launch"},
+               "l2": "%d distinct layer copies, %.0f MB of algorithmic bytes per step (> L2)" % (
+                   ng * gl, float(bytes_step.mean()) / 1e6),
+               "algorithmic_MB_per_step": round(float(bytes_step.mean()) / 1e6, 2)}, args=args),
+           "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
+                          "p99": float(np.percentile(per_step, 99))},
+           "roofline": roofline, "phases_us": None, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": int(args.steps), "clocks": clk}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     maybe_spawn(args)
@@ -396,6 +503,10 @@ def main():
     from paper_2312_12456_b200.stack import algorithmic_bytes, build_stack
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1 and n_layers == 1 and not args.no_group and B == 1:
+        torch.cuda.set_device(0)
+        run_grouped(args, cfg, B, torch.device("cuda", 0))
+        return
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)

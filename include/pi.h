@@ -245,6 +245,28 @@ pi_status pi_stack_run(pi_stack *S, const float *x, int32_t B, float *y, int32_t
 pi_status pi_stack_run_host(pi_stack *S, const float *x_host, int32_t B, float *y_host,
                             pi_stream_t stream);
 
+/* A group: n_groups INDEPENDENT decode problems in ONE persistent launch -- the throughput form
+ * of the per-layer operator for layers too small to keep the whole GPU streaming on their own
+ * (single-layer decode measured over many layer copies; "the operator ...
+ * computes each neuron independently").  The SMs are split into n_groups groups of
+ * group_ctas CTAs; group k runs layers[k * n_layers .. (k + 1) * n_layers) as a stack (x_{l+1} =
+ * y_l) on its own input with grid barriers local to the group, so the groups' predictor,
+ * synchronisation and FFN phases overlap and HBM stays busy.  Every layer must share layer 0's
+ * shape, dtype, act, pred_act and flags, with 16-bit FFN rows and no speculative prefix;
+ * n_groups * group_ctas <= SMs; the handle owns its own workspace (the layers' workspaces are
+ * not used) and keeps pointers to the layers (destroy it before them).  Errors:
+ * INVALID_ARGUMENT, SHAPE, UNSUPPORTED (no grouped kernel for the shape, e.g. r > 64 group_ctas),
+ * OUT_OF_MEMORY, CUDA. */
+typedef struct pi_group pi_group;
+pi_status pi_group_create(pi_layer *const *layers, int32_t n_groups, int32_t n_layers, int32_t group_ctas,
+                          pi_group **out);
+pi_status pi_group_destroy(pi_group *G);
+/* One step of every group: x, y dev fp32 [n_groups, B, d] (group k reads x[k], writes y[k]);
+ * B must be 1; n_active_out: dev int32 [n_groups, n_layers] or NULL.  Graph capturable.
+ * Errors: INVALID_ARGUMENT, UNSUPPORTED, ALIGNMENT (x, y 16-B aligned), CUDA. */
+pi_status pi_group_run(pi_group *G, const float *x, int32_t B, float *y, int32_t *n_active_out,
+                       pi_stream_t stream);
+
 /* Profiling aid (tracing): when dev_buf is non-NULL, every later pi_layer_forward that runs
  * the fused kernel has each CTA's thread 0 write globaltimer (ns) stamps of its phase
  * boundaries to dev_buf[cta * 256 + k]: 0 start, 1 P1 done, 2 after grid barrier 1, 3 P2 done,

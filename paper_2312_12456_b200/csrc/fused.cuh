@@ -325,14 +325,15 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     }
     __syncwarp();
     if (lane == 0) {
-      // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping)
+      // every ring use gets kConsumerWarps arrivals on `empty` and one on `hready` (phase bookkeeping).
+      // Jobs are dealt round-robin, so the stage's jobs_here jobs touch nw = min(16, jobs_here) warps;
+      // each of them arrives once, after its last job on the stage (jj + 16 >= jobs_here), and the warp
+      // holding the jobs jj = 0 mod 16 also arrives for the 16 - nw warps with no job here.
       const int jobs_here = 4 * (min(nwords, (st + 1) * wpp) - st * wpp);
-      if (jj == 0) {
-        mbar_arrive_cnt(&x.hready[slot], 32);
-        mbar_arrive_cnt(&x.empty[slot], kConsumerWarps - jobs_here + 1);
-      } else {
-        mbar_arrive(&x.empty[slot]);
-      }
+      const int nw = min(kConsumerWarps, jobs_here);
+      if (jj == 0) mbar_arrive_cnt(&x.hready[slot], 32);
+      if (jj + kConsumerWarps >= jobs_here)
+        mbar_arrive_cnt(&x.empty[slot], 1 + ((jj % kConsumerWarps == 0) ? kConsumerWarps - nw : 0));
     }
     if (dt && first_job) dt[48 + warp] = globaltimer();
     first_job = false;
@@ -422,13 +423,38 @@ __device__ __forceinline__ void spec_down_stage(float (&yr)[CH][8][B], const uin
 // default kernel carries none of its code (it costs registers: measured slower).
 // Q4: the FFN rows are INT4 records (PI_FFN_Q4, row f3; B = 1): a thread's 8-element chunk of d is
 // one 32-bit word of codes and one fp16 scale, dequantised in registers (w = s (q - 8)).
-template <typename T, int B, bool REGLU, int CH, int NA, bool SPEC, bool Q4>
-__global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p) {
-  constexpr int RPM = (NA == 1) ? 2 : 8;      // max P1 rows per stage
+// Grouped launch (GRP, pi_group_run): group k of the grid sees its own layers, input, output and
+// slice of every workspace buffer (fused_alloc with groups > 1 lays them out with these strides).
+__device__ __forceinline__ FusedParams group_view(const FusedParams &a, int k, int P) {
+  FusedParams p = a;
+  const size_t K = (size_t)k;
+  p.lws = a.lws + K * a.L;
+  p.x = a.x + K * a.B * a.d;
+  p.y = a.y + K * a.B * a.d;
+  p.xbuf = a.xbuf + K * kFusedMaxB * a.d;
+  p.g = a.g + K * kFusedMaxB * a.r;
+  p.ypart = a.ypart + K * P * kFusedMaxB * a.d;
+  p.counts = a.counts + K * P;
+  p.counts_full = a.counts_full + K * P;
+  p.mask = a.mask + K * kFusedMaxB * a.words;
+  p.uni = a.uni + K * a.words;
+  p.bar = a.bar + K * (size_t)(P + 2) * 16;
+  p.n_out = a.n_out ? a.n_out + K * a.L : nullptr;
+  p.ids_out = nullptr;
+  if (k) p.trace = nullptr;
+  return p;
+}
+
+template <typename T, int B, bool REGLU, int CH, int NA, bool SPEC, bool Q4, bool GRP = false>
+__global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0) {
+  constexpr int RPM = fused_rpm(CH);          // max P1 rows per stage (fused_geometry)
   extern __shared__ __align__(128) uint8_t fsmem[];
   uint8_t *smem = fsmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int P = gridDim.x, c = blockIdx.x;
+  const int P = GRP ? p0.group_ctas : (int)gridDim.x;
+  const int grp = GRP ? (int)blockIdx.x / P : 0;
+  const int c = GRP ? (int)blockIdx.x - grp * P : (int)blockIdx.x;
+  const FusedParams p = GRP ? group_view(p0, grp, P) : p0;
   const int d = p.d, r = p.r, m = p.m, L = p.L;
   const int NS = p.NS, SB = p.stage_bytes, G = p.G, RP1 = p.rows_p1;
 
@@ -460,7 +486,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
   __shared__ int s_ncorr, s_count_full;
   __shared__ __align__(8) uint64_t s_b2_arrive, s_b2_done;   // SPEC: split-phase grid barrier 2
   __shared__ float s_ss[kGroupWarps][B];
-  __shared__ float s_b1[16];
+  __shared__ float s_b1[kMaxP1PerCta];
   __shared__ int s_n, s_k0, s_k1, s_count;
   unsigned long long *trace = p.trace ? p.trace + (size_t)c * 256 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
@@ -1207,10 +1233,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
     {
       const int j0 = (int)(((int64_t)c * d) / P), j1 = (int)(((int64_t)(c + 1) * d) / P);
       const int ncol = j1 - j0;
-      constexpr int SPL = 8;    // partial groups summed separately, then combined in order
       constexpr int PPG = 32;   // partials per group (P <= 256)
       float *part = s_part;     // [SPL][ncol*B]
       const int items = ncol * B;
+      // partial groups summed separately, then combined in order: 8 for the full grid (P = 148:
+      // ~56 columns per CTA), fewer when a small group of CTAs owns many columns (grouped launch),
+      // so every thread's loads stay one round trip; at least ceil(P / PPG) groups
+      const int SPL = GRP ? max((P + PPG - 1) / PPG, min(8, kConsumers / max(1, items))) : 8;
       for (int idx = tid; idx < items * SPL; idx += kConsumers) {
         const int sgp = idx / items, it2 = idx % items;
         const int b = it2 / ncol, j = j0 + it2 % ncol;
@@ -1227,7 +1256,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
       for (int it2 = tid; it2 < items; it2 += kConsumers) {
         const int b = it2 / ncol, j = j0 + it2 % ncol;
         float acc = 0.f;
-#pragma unroll
         for (int sgp = 0; sgp < SPL; ++sgp) acc += part[sgp * items + it2];
         if (lw.b_down) acc += WT<T>::to_float(lw.b_down, j);
         yout[(size_t)b * d + j] = acc;
@@ -1242,16 +1270,31 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p)
 template <typename T, int B, bool REGLU, int CH, int NA>
 inline cudaError_t fused_launch_t(const FusedWork &w, const FusedParams &prm, cudaStream_t s) {
   auto kern = k_layer<T, B, REGLU, CH, NA, false, false>;
-  if constexpr (CH <= 4) {   // the speculative variant is instantiated for d <= 8192 only
+  int grid = w.P;
+  if (prm.group_ctas > 0) {   // grouped launch: B = 1, d <= 8192, 16-bit rows (fused_group_supported)
+    if constexpr (B == 1 && (CH <= 2 || (CH <= 4 && NA == 1))) {
+      kern = k_layer<T, B, REGLU, CH, NA, false, false, true>;
+      grid = w.P * w.groups;
+    } else {
+      return cudaErrorNotSupported;
+    }
+  }
+  if (prm.group_ctas > 0 && (prm.spec || prm.rec_q4 > 0)) return cudaErrorNotSupported;
+  // the speculative variant: d <= 8192, one or eight neurons per stage (other shapes run unspeculated,
+  // which gives the same result: the default kernel ignores the speculative tables)
+  if constexpr (CH <= 4 && (NA == 1 || NA == 8)) {
     if (prm.spec) kern = k_layer<T, B, REGLU, CH, NA, true, false>;
   }
-  if constexpr (B == 1) {    // INT4 rows (the speculative variant is 16-bit only)
+  // INT4 rows (B = 1; 16-bit kernels only otherwise): the (CH, NA) shapes fused_geometry picks for records
+  if constexpr (B == 1 && ((CH <= 2 && NA >= 4) || (CH >= 3 && CH <= 4 && NA == 4) || (CH >= 5 && NA == 2))) {
     if (prm.rec_q4 > 0) kern = k_layer<T, B, REGLU, CH, NA, false, true>;
+  } else {
+    if (prm.rec_q4 > 0) return cudaErrorNotSupported;
   }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, w.smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(w.P);
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kFusedThreads);
   cfg.dynamicSmemBytes = (size_t)w.smem;
   cfg.stream = s;
@@ -1268,10 +1311,10 @@ template <typename T, int B, bool RG>
 cudaError_t fused_launch_tbr(const FusedWork &w, const FusedParams &p, int CH, int NA, cudaStream_t s) {
 #define PI_FL(CHV, NAV) \
   if (CH == CHV && NA == NAV) return fused_launch_t<T, B, RG, CHV, NAV>(w, p, s);
-  PI_FL(1, 8) PI_FL(1, 1) PI_FL(2, 8) PI_FL(2, 1) PI_FL(3, 1) PI_FL(4, 1)
+  PI_FL(1, 8) PI_FL(1, 4) PI_FL(1, 2) PI_FL(1, 1) PI_FL(2, 8) PI_FL(2, 4) PI_FL(2, 2) PI_FL(2, 1) PI_FL(3, 1) PI_FL(4, 1)
   if constexpr (B == 1) {   // wider d keeps x and y register-resident only for one token
     PI_FL(5, 1) PI_FL(6, 1) PI_FL(7, 1) PI_FL(8, 1)
-    PI_FL(3, 4) PI_FL(4, 4) PI_FL(6, 4)   // INT4 rows, 2-4 neurons per stage
+    PI_FL(3, 4) PI_FL(4, 4) PI_FL(5, 2) PI_FL(6, 2) PI_FL(7, 2) PI_FL(8, 2)   // INT4 rows, 2-4 neurons per stage
   }
 #undef PI_FL
   return cudaErrorNotSupported;

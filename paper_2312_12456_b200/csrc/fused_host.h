@@ -46,11 +46,12 @@ constexpr int kConsumers = kConsumerWarps * 32;       // 512
 constexpr int kFusedThreads = kConsumers + 32;        // + producer warp
 constexpr int kFusedMaxB = 2;
 constexpr int kMaxCH = 8;        // 16-byte chunks of d per group thread (d <= 16384)
-constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage
+constexpr int kMaxWordsP2 = 16;  // P2 mask words per stage (4 jobs per word: 2 row tiles x 2 K halves)
 constexpr int kRedStride = 32;   // floats per warp in the up-group reduction buffer
 constexpr int kMaxStages = 16;   // ring stages (s_slot_pos)
 constexpr int kMaxSpecPerCta = 32;   // speculative hot-prefix neurons per CTA (static shared tables)
 constexpr int kMaxCorrPerCta = 32;   // corrections per CTA and layer (more: the rest run unspeculated)
+constexpr int kMaxP1PerCta = 64;     // predictor hidden rows per CTA (s_b1)
 
 struct FusedWork {
   bool enabled = false;
@@ -67,6 +68,7 @@ struct FusedWork {
   uint32_t *uni = nullptr;            // [words]
   float *xbuf = nullptr;              // [maxB, d] inter-layer activations (stack launch)
   unsigned long long *trace = nullptr;  // optional phase trace (pi_layer_set_trace)
+  int groups = 1;                     // grouped workspace (pi_group): buffers repeated per group
 };
 
 struct FusedArgs {
@@ -115,6 +117,9 @@ struct FusedParams {
   int rec_q4;                 // INT4 FFN records (bytes per neuron and matrix); 0 = 16-bit rows
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int hot_cap;                // at most this many hot neurons are L2-prefetched per layer
+  int group_ctas;             // > 0: grouped launch (pi_group_run) -- the grid is n_groups independent
+                              // problems of group_ctas CTAs each; group k uses lws + k L, x/y + k B d and
+                              // the k-th slice of every workspace buffer (strides: fused.cuh group_view)
 };
 
 // Everything below is host code (kernel launch parameters, workspace sizing, dispatch); the
@@ -126,22 +131,26 @@ inline int fused_ch(int d) { return (d / 8 + kGroup - 1) / kGroup; }
 
 template <class Alloc>
 inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc,
-                        int rec_q4 = 0) {
+                        int rec_q4 = 0, int groups = 1) {
   w = FusedWork{};
+  w.groups = groups;
   w.rec_q4 = rec_q4;
   w.d = d;
   w.m = m;
   w.r = r;
   w.reglu = reglu;
   const int ch = fused_ch(d);
-  if (ch > kMaxCH || d < 8 || r > 16 * num_sms || num_sms > 256)
+  if (ch > kMaxCH || d < 8 || r > kMaxP1PerCta * num_sms || num_sms > 256)
     return true;  // unsupported shape: stays disabled (per-step kernels)
   w.P = num_sms;
   w.kt = (r + 15) / 16;
   const size_t p2_word = (size_t)32 * w.kt * 16 * 2;   // one 32-row word of the tiled P2
-  // stage: >= one neuron (gate|up + down), one P2 word, >= 32 KB
+  // stage: >= one P2 word, >= 32 KB, and a whole number NA of neurons (gate|up + down; NA a power of
+  // two <= 8, as many as ~40 KB hold) so no neuron slot of the instantiated kernel idles
   const size_t nb = rec_q4 ? (size_t)rec_q4 * (reglu ? 3 : 2) : (size_t)d * (reglu ? 6 : 4);
-  size_t sb = std::max<size_t>({(size_t)32 * 1024, nb, p2_word});
+  size_t na = 1;
+  while (na < 8 && 2 * na * nb <= (size_t)(rec_q4 ? 48 : 40) * 1024) na *= 2;
+  size_t sb = std::max<size_t>({(size_t)32 * 1024, na * nb, p2_word});
   sb = (sb + 127) / 128 * 128;
   // compaction stages the union words, the per-token words and the P counts in one ring slot
   if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)2 * num_sms * 4 > sb) return true;
@@ -151,50 +160,58 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const int words_all = (m + 31) / 32;
   w.wcap = (words_all + w.P - 1) / w.P + 1;
   w.pcap = (d + w.P - 1) / w.P + 1;
-  constexpr int NT = (3 * kFusedMaxB + 7) / 8;
+  const int mb = std::max(1, std::min(maxB, kFusedMaxB));   // the kernel's B <= max_batch
+  const int NT = (3 * mb + 7) / 8;
   // everything but the ring: mbarriers, reduction buffers, h, logits, b2, b_up/ids/bits, phase-4
   // partials, g staging and its B fragments; the ring gets the rest (<= 200 KB)
   auto extras = [&](int ns) {
-    return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * kFusedMaxB * 4 +
-           (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * kFusedMaxB * 4 +
-           (size_t)kFusedMaxB * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
+    return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * mb * 4 +
+           (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * mb * 4 +
+           (size_t)mb * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
   };
   const size_t cap = 227 * 1024 - 2560;   // static shared memory (speculative tables, barriers) and slack
   w.NS = (int)std::min<size_t>({200 * 1024 / sb, cap / sb, (size_t)kMaxStages});
-  if ((size_t)w.kt * 12 * kFusedMaxB > (size_t)3 * kConsumers) return true;   // p2_phase: <= 3 entries per thread
+  if ((size_t)w.kt * 12 * mb > (size_t)3 * kConsumers) return true;   // p2_phase: <= 3 entries per thread
   while (w.NS >= 2 && (size_t)w.NS * sb + extras(w.NS) > cap) --w.NS;
   if (w.NS < 2) return true;
   const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
-                     (size_t)w.NS * 8 * kFusedMaxB * 4 + (size_t)(2 * kFusedMaxB + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
+                     (size_t)w.NS * 8 * mb * 4 + (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
   w.part_off = (int)(((size_t)w.NS * sb + pre + 15) / 16 * 16);
-  w.smem = w.part_off + 8 * w.pcap * kFusedMaxB * 4 + kFusedMaxB * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
+  w.smem = w.part_off + 8 * w.pcap * mb * 4 + mb * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
   const int words = (m + 31) / 32;
-  if (!alloc((void **)&w.bar, (size_t)(1 + num_sms) * 128 + 128)) return false;
-  if (!alloc((void **)&w.g, (size_t)maxB * r * 4)) return false;
-  if (!alloc((void **)&w.ypart, (size_t)w.P * std::min(maxB, kFusedMaxB) * d * 4)) return false;
-  if (!alloc((void **)&w.counts, (size_t)w.P * 4)) return false;
-  if (!alloc((void **)&w.counts_full, (size_t)w.P * 4)) return false;
-  if (!alloc((void **)&w.mask, (size_t)maxB * words * 4)) return false;
-  if (!alloc((void **)&w.uni, (size_t)words * 4)) return false;
-  if (!alloc((void **)&w.xbuf, (size_t)std::min(maxB, kFusedMaxB) * d * 4)) return false;
+  // a grouped workspace repeats every buffer per group with the strides of fused.cuh group_view
+  const size_t G = (size_t)groups;
+  const int gb = groups > 1 ? kFusedMaxB : maxB;
+  if (!alloc((void **)&w.bar, G * ((size_t)(1 + num_sms) * 128 + 128))) return false;
+  if (!alloc((void **)&w.g, G * (size_t)gb * r * 4)) return false;
+  if (!alloc((void **)&w.ypart, G * (size_t)w.P * std::min(gb, kFusedMaxB) * d * 4)) return false;
+  if (!alloc((void **)&w.counts, G * (size_t)w.P * 4)) return false;
+  if (!alloc((void **)&w.counts_full, G * (size_t)w.P * 4)) return false;
+  if (!alloc((void **)&w.mask, G * (size_t)gb * words * 4)) return false;
+  if (!alloc((void **)&w.uni, G * (size_t)words * 4)) return false;
+  if (!alloc((void **)&w.xbuf, G * (size_t)std::min(gb, kFusedMaxB) * d * 4)) return false;
   if (w.smem > 227 * 1024) return true;
   w.enabled = true;
   return true;
 }
 
 inline void fused_init(FusedWork &w, cudaStream_t s) {
-  if (w.enabled) cudaMemsetAsync(w.bar, 0, (size_t)(1 + w.P) * 128 + 128, s);
+  if (w.enabled) cudaMemsetAsync(w.bar, 0, (size_t)w.groups * ((size_t)(1 + w.P) * 128 + 128), s);
 }
+
+// max P1 rows per stage of the kernel (its unrolled row loop): ~one 32 KB stage of d-rows
+__host__ __device__ constexpr int fused_rpm(int ch) { return ch >= 8 ? 1 : (8 / ch > 8 ? 8 : 8 / ch); }
 
 // neurons per stage (NA template bound and runtime G) and P1 rows per stage
 inline void fused_geometry(const FusedWork &w, int d, bool reglu, int *NA, int *G, int *RP1) {
   const size_t nb = w.rec_q4 ? (size_t)w.rec_q4 * (reglu ? 3 : 2) : (size_t)d * 2 * (reglu ? 3 : 2);
-  const int g = (int)(w.stage_bytes / nb);
-  // 8 neurons per stage when they fit; INT4 rows of wide layers (2-4 per stage) use the 4 variant
-  *NA = g >= 2 ? ((w.rec_q4 && g <= 4) ? 4 : 8) : 1;
-  *G = std::min(*NA, std::max(1, g));
+  const int g = (int)std::min<size_t>(8, w.stage_bytes / nb);
+  // neurons per stage: the largest power of two <= 8 the stage holds (the kernel's unrolled
+  // neuron loop is exactly NA long, so no slot computes on padding)
+  *NA = g >= 8 ? 8 : g >= 4 ? 4 : g >= 2 ? 2 : 1;
+  *G = *NA;
   const int rp = (int)(w.stage_bytes / ((size_t)d * 2));
-  *RP1 = std::max(1, std::min(*NA == 1 ? 2 : 8, rp));
+  *RP1 = std::max(1, std::min(fused_rpm(fused_ch(d)), rp));
 }
 
 inline bool fused_supported(const FusedWork &w, int B = 1) {
@@ -205,9 +222,20 @@ inline bool fused_supported(const FusedWork &w, int B = 1) {
   int NA, G, RP1;
   fused_geometry(w, w.d, w.reglu, &NA, &G, &RP1);
   // the instantiated (CH, NA) combinations (fused_launch_tbr)
-  if (NA == 4) return B == 1 && (ch == 3 || ch == 4 || ch == 6);
+  if (w.rec_q4)   // INT4 records: fused.cuh fused_launch_t's Q4 list
+    return (ch <= 2 && NA >= 4) || ((ch == 3 || ch == 4) && NA == 4) || (ch >= 5 && NA == 2);
   if (ch <= 2) return true;
-  return NA == 1 && (ch <= 4 || (B == 1 && ch <= kMaxCH));
+  if (NA == 1) return ch <= 4 || (B == 1 && ch <= kMaxCH);
+  return false;
+}
+
+// the grouped kernel (fused.cuh fused_launch_t) is instantiated for B = 1, d <= 8192 (CH <= 4), NA 1 or 8
+inline bool fused_group_supported(const FusedWork &w) {
+  if (!w.enabled || w.rec_q4) return false;
+  int NA, G, RP1;
+  fused_geometry(w, w.d, w.reglu, &NA, &G, &RP1);
+  const int ch = fused_ch(w.d);
+  return ch <= 2 || (ch <= 4 && NA == 1);
 }
 
 // One instantiation unit per (weight type, batch, activation): fused_inst_<T>_b<B>_<act>.cu

@@ -528,6 +528,131 @@ extern "C" pi_status pi_stack_run_host(pi_stack *S, const float *x_host, int32_t
   return PI_OK;
 }
 
+// ---------------------------------------------------------------------------
+// groups: n_groups independent stacks in ONE persistent launch (SMs split into groups)
+// ---------------------------------------------------------------------------
+struct pi_group {
+  std::vector<pi_layer *> layers;   // [n_groups * n_layers], group-major
+  int n_groups = 0, n_layers = 0, group_ctas = 0;
+  LayerW *lws = nullptr;            // device [n_groups * n_layers]
+  FusedWork fw{};                   // geometry for P = group_ctas, buffers repeated per group
+  std::vector<void *> allocs;
+};
+
+static void group_free(pi_group *G) {
+  if (!G) return;
+  for (void *p : G->allocs) cudaFree(p);
+  if (G->lws) cudaFree(G->lws);
+  delete G;
+}
+
+extern "C" pi_status pi_group_create(pi_layer *const *layers, int32_t n_groups, int32_t n_layers,
+                                     int32_t group_ctas, pi_group **out) {
+  g_err.clear();
+  if (!out) return fail(PI_ERR_INVALID_ARGUMENT, "group: out is NULL");
+  *out = nullptr;
+  if (!layers || n_groups < 1 || n_layers < 1)
+    return fail(PI_ERR_INVALID_ARGUMENT, "group: NULL layers, n_groups < 1 or n_layers < 1");
+  const pi_layer *L0 = layers[0];
+  if (!L0) return fail(PI_ERR_INVALID_ARGUMENT, "group: layer 0 is NULL");
+  const int total = n_groups * n_layers;
+  for (int i = 0; i < total; ++i) {
+    const pi_layer *Ll = layers[i];
+    if (!Ll) return fail(PI_ERR_INVALID_ARGUMENT, "group: layer %d is NULL", i);
+    if (Ll->d != L0->d || Ll->m_local != L0->m_local || Ll->r != L0->r || Ll->act != L0->act ||
+        Ll->dtype != L0->dtype || Ll->pred_act != L0->pred_act || Ll->flags != L0->flags ||
+        Ll->device != L0->device || Ll->ffn != L0->ffn || Ll->n_spec != L0->n_spec)
+      return fail(PI_ERR_SHAPE, "group: layer %d (id %d) differs from layer 0 in shape/dtype/act/flags/format", i,
+                  Ll->layer_id);
+  }
+  if (L0->ffn != PI_FFN_16 || L0->n_spec > 0)
+    return fail(PI_ERR_UNSUPPORTED, "group: grouped launches take 16-bit FFN rows without a speculative prefix");
+  if (group_ctas < 1 || (int64_t)group_ctas * n_groups > L0->num_sms)
+    return fail(PI_ERR_INVALID_ARGUMENT, "group: n_groups %d x group_ctas %d exceeds the %d SMs", n_groups,
+                group_ctas, L0->num_sms);
+  pi_group *G = new pi_group();
+  G->layers.assign(layers, layers + total);
+  G->n_groups = n_groups;
+  G->n_layers = n_layers;
+  G->group_ctas = group_ctas;
+  auto alloc = [&](void **p, size_t bytes) {
+    if (cudaMalloc(p, bytes) != cudaSuccess) return false;
+    G->allocs.push_back(*p);
+    return true;
+  };
+  if (!fused_alloc(G->fw, L0->d, L0->m_local, L0->r, 1, group_ctas, L0->act == PI_ACT_REGLU, alloc, 0,
+                   n_groups)) {
+    group_free(G);
+    return fail(PI_ERR_OUT_OF_MEMORY, "group: workspace");
+  }
+  if (!fused_supported(G->fw, 1) || !fused_group_supported(G->fw)) {
+    group_free(G);
+    return fail(PI_ERR_UNSUPPORTED, "group: shape d=%d m=%d r=%d has no grouped fused kernel for %d CTAs per group",
+                L0->d, L0->m_local, L0->r, group_ctas);
+  }
+  std::vector<LayerW> h(total);
+  for (int i = 0; i < total; ++i) {
+    const pi_layer *Ll = layers[i];
+    h[i] = LayerW{};
+    h[i].w_up = (const uint8_t *)Ll->w_up;
+    h[i].w_down = (const uint8_t *)Ll->w_down;
+    h[i].p_w1 = (const uint8_t *)Ll->p_w1;
+    h[i].p_w2 = (const uint8_t *)Ll->p_w2;
+    h[i].b_up = Ll->b_up;
+    h[i].b_down = Ll->b_down;
+    h[i].p_b1 = Ll->p_b1;
+    h[i].p_b2 = Ll->p_b2;
+    h[i].t = Ll->threshold;
+    h[i].hot_ids = Ll->hot_ids;
+    h[i].n_hot = std::min(Ll->n_hot, Ll->hot_cap);
+  }
+  if (cudaMalloc(&G->lws, sizeof(LayerW) * total) != cudaSuccess ||
+      cudaMemcpy(G->lws, h.data(), sizeof(LayerW) * total, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(G->fw.bar, 0, (size_t)n_groups * ((size_t)(1 + group_ctas) * 128 + 128)) != cudaSuccess) {
+    group_free(G);
+    return fail(PI_ERR_CUDA, "group: layer table / barrier init");
+  }
+  *out = G;
+  return PI_OK;
+}
+
+extern "C" pi_status pi_group_destroy(pi_group *G) {
+  g_err.clear();
+  if (!G) return PI_OK;
+  cudaDeviceSynchronize();
+  group_free(G);
+  return PI_OK;
+}
+
+extern "C" pi_status pi_group_run(pi_group *G, const float *x, int32_t B, float *y, int32_t *n_active_out,
+                                  pi_stream_t stream) {
+  g_err.clear();
+  if (!G) return fail(PI_ERR_INVALID_ARGUMENT, "group handle is NULL");
+  if (!x || !y) return fail(PI_ERR_INVALID_ARGUMENT, "group: NULL x or y");
+  if (B != 1) return fail(PI_ERR_UNSUPPORTED, "group: grouped launches run B = 1 (got %d)", B);
+  if (!aligned16(x) || !aligned16(y)) return fail(PI_ERR_ALIGNMENT, "group: x and y must be 16-B aligned");
+  pi_layer *L0 = G->layers[0];
+  return dispatch_t(L0->dtype, [&](auto tt) {
+    using T = typename decltype(tt)::type;
+    FusedArgs a{};
+    a.x = x; a.y = y; a.d = L0->d; a.m = L0->m_local; a.r = L0->r; a.words = L0->words; a.B = B;
+    a.threshold = L0->threshold; a.rmsnorm = (L0->flags & PI_FLAG_INPUT_RMSNORM) != 0;
+    a.pred_relu = L0->pred_act == PI_PRED_RELU; a.reglu = L0->act == PI_ACT_REGLU;
+    a.n_out = n_active_out;
+    a.hot_cap = L0->hot_cap;
+    FusedParams p = fused_params(G->fw, a);
+    p.lws = G->lws;
+    p.L = G->n_layers;
+    p.mask = G->fw.mask;
+    p.ids_out = nullptr;
+    p.trace = L0->fw.trace;      // pi_layer_set_trace on layer 0: group 0's CTAs stamp their phases
+    p.group_ctas = G->group_ctas;
+    cudaError_t e = fused_launch_p<T>(G->fw, p, a.reglu, B, (cudaStream_t)stream);
+    if (e != cudaSuccess) return fail(PI_ERR_CUDA, "group: fused launch: %s", cudaGetErrorString(e));
+    return PI_OK;
+  });
+}
+
 extern "C" pi_status pi_layer_set_trace(pi_layer *L, uint64_t *dev_buf) {
   g_err.clear();
   if (!L) return fail(PI_ERR_INVALID_ARGUMENT, "layer handle is NULL");

@@ -36,7 +36,8 @@ PI_MAX_BATCH = 32
 EXPORTS = ("pi_version", "pi_last_error", "pi_layer_create", "pi_layer_destroy", "pi_layer_get_info",
            "pi_predict", "pi_compact", "pi_sparse_ffn", "pi_layer_forward", "pi_layer_forward_host",
            "pi_stack_forward", "pi_stack_forward_host", "pi_partition", "pi_layer_set_trace",
-           "pi_stack_create", "pi_stack_destroy", "pi_stack_run", "pi_stack_run_host", "pi_place_ilp")
+           "pi_stack_create", "pi_stack_destroy", "pi_stack_run", "pi_stack_run_host", "pi_place_ilp",
+           "pi_group_create", "pi_group_destroy", "pi_group_run")
 
 
 class PiError(RuntimeError):
@@ -95,6 +96,9 @@ def _load() -> ctypes.CDLL:
     lib.pi_stack_destroy.argtypes = [vp]
     lib.pi_stack_run.argtypes = [vp, vp, i32, vp, vp, vp]
     lib.pi_stack_run_host.argtypes = [vp, vp, i32, vp, vp]
+    lib.pi_group_create.argtypes = [P(vp), i32, i32, i32, P(vp)]
+    lib.pi_group_destroy.argtypes = [vp]
+    lib.pi_group_run.argtypes = [vp, vp, i32, vp, vp, vp]
     dbl = ctypes.c_double
     lib.pi_place_ilp.argtypes = [vp, i32, i32, vp, i32, dbl, dbl, dbl, dbl, vp, vp, ctypes.POINTER(dbl)]
     for name in EXPORTS:
@@ -299,6 +303,38 @@ class StackHandle:
             pass
 
 
+class GroupHandle:
+    """Owns a pi_group: n_groups independent stacks of n_layers layers in ONE persistent launch,
+    group_ctas CTAs per group (include/pi.h).  x, y: [n_groups, 1, d] device fp32."""
+
+    def __init__(self, groups: Sequence[Sequence[Layer]], group_ctas: int):
+        self.layers = [L for g in groups for L in g]
+        self.n_groups, self.n_layers = len(groups), len(groups[0])
+        assert all(len(g) == self.n_layers for g in groups)
+        arr = handles(self.layers)
+        h = ctypes.c_void_p()
+        _check(_lib.pi_group_create(arr, self.n_groups, self.n_layers, group_ctas, ctypes.byref(h)))
+        self.handle = h
+        self.group_ctas = group_ctas
+
+    def run(self, x, y, n_active_out=None, stream=None):
+        assert x.shape[0] == self.n_groups and y.shape[0] == self.n_groups
+        _check(_lib.pi_group_run(self.handle, _ptr(x), x.shape[1], _ptr(y), _ptr(n_active_out), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None:
+            _lib.pi_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+pi_group_create = GroupHandle
+pi_group_run = GroupHandle.run
 pi_stack_create = StackHandle
 pi_stack_run = StackHandle.run
 pi_stack_run_host = StackHandle.run_host
