@@ -472,8 +472,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
   float *s_bup = s_b2 + p.wcap * 32;                                 // [idcap]
   int *s_ids = reinterpret_cast<int *>(s_bup + p.idcap);             // [idcap]
   uint8_t *s_bits = reinterpret_cast<uint8_t *>(s_ids + p.idcap);    // [idcap]
-  float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // [8][pcap*B] phase-4 partials
-  float *sg = s_part + 8 * p.pcap * B;                               // [B][kt*16] staging of g
+  float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // phase-4 partial sums (fused_spart)
+  float *sg = s_part + fused_spart(P, p.pcap, B);                    // [B][kt*16] staging of g
   uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
   __shared__ unsigned s_gmax[B];
   __shared__ uint32_t s_slot_pos[kMaxStages];
@@ -1230,35 +1230,47 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
     if (tr && tid == 0) tr[7] = globaltimer();
 
     // ---------------- phase 4: y[:, cols of CTA c] = sum over P partials + b_down ----------------
+    // CTA c owns the 8-column units [u0, u1) of d (32-byte sectors).  Work item = (group of <= 8
+    // partials, 4-column chunk, token): one 16-byte load per partial, all of a thread's loads in
+    // flight at once; the group sums are combined in ascending group order (fixed order).
     {
-      const int j0 = (int)(((int64_t)c * d) / P), j1 = (int)(((int64_t)(c + 1) * d) / P);
-      const int ncol = j1 - j0;
-      constexpr int PPG = 32;   // partials per group (P <= 256)
-      float *part = s_part;     // [SPL][ncol*B]
-      const int items = ncol * B;
-      // partial groups summed separately, then combined in order: 8 for the full grid (P = 148:
-      // ~56 columns per CTA), fewer when a small group of CTAs owns many columns (grouped launch),
-      // so every thread's loads stay one round trip; at least ceil(P / PPG) groups
-      const int SPL = GRP ? max((P + PPG - 1) / PPG, min(8, kConsumers / max(1, items))) : 8;
+      constexpr int PPG = 8;    // partials per group
+      const int u0 = (int)(((int64_t)c * (d >> 3)) / P), u1 = (int)(((int64_t)(c + 1) * (d >> 3)) / P);
+      const int nq = 2 * (u1 - u0);            // 4-column chunks of this CTA
+      const int items = nq * B;
+      const int SPL = max((P + PPG - 1) / PPG, min(32, kConsumers / max(1, items)));
+      float4 *part = reinterpret_cast<float4 *>(s_part);   // [SPL][items]
       for (int idx = tid; idx < items * SPL; idx += kConsumers) {
-        const int sgp = idx / items, it2 = idx % items;
-        const int b = it2 / ncol, j = j0 + it2 % ncol;
+        const int sgp = idx / items, it2 = idx - sgp * items;
+        const int b = it2 / nq, j = u0 * 8 + (it2 - b * nq) * 4;
         const int c0 = (sgp * P) / SPL, c1 = ((sgp + 1) * P) / SPL;
-        float v[PPG];
+        float4 v[PPG];
 #pragma unroll
-        for (int q = 0; q < PPG; ++q) v[q] = (c0 + q < c1) ? __ldcg(p.ypart + ((size_t)(c0 + q) * B + b) * d + j) : 0.f;
-        float acc = 0.f;
+        for (int q = 0; q < PPG; ++q)
+          v[q] = (c0 + q < c1) ? __ldcg(reinterpret_cast<const float4 *>(p.ypart + ((size_t)(c0 + q) * B + b) * d + j))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 acc = v[0];
 #pragma unroll
-        for (int q = 0; q < PPG; ++q) acc += v[q];
+        for (int q = 1; q < PPG; ++q) {
+          acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w;
+        }
         part[sgp * items + it2] = acc;
       }
       consumers_sync();
       for (int it2 = tid; it2 < items; it2 += kConsumers) {
-        const int b = it2 / ncol, j = j0 + it2 % ncol;
-        float acc = 0.f;
-        for (int sgp = 0; sgp < SPL; ++sgp) acc += part[sgp * items + it2];
-        if (lw.b_down) acc += WT<T>::to_float(lw.b_down, j);
-        yout[(size_t)b * d + j] = acc;
+        const int b = it2 / nq, j = u0 * 8 + (it2 - b * nq) * 4;
+        float4 acc = part[it2];
+        for (int sgp = 1; sgp < SPL; ++sgp) {
+          const float4 w4 = part[sgp * items + it2];
+          acc.x += w4.x; acc.y += w4.y; acc.z += w4.z; acc.w += w4.w;
+        }
+        if (lw.b_down) {
+          acc.x += WT<T>::to_float(lw.b_down, j);
+          acc.y += WT<T>::to_float(lw.b_down, j + 1);
+          acc.z += WT<T>::to_float(lw.b_down, j + 2);
+          acc.w += WT<T>::to_float(lw.b_down, j + 3);
+        }
+        *reinterpret_cast<float4 *>(yout + (size_t)b * d + j) = acc;
       }
     }
     if (tr && tid == 0) tr[8] = globaltimer();

@@ -128,6 +128,10 @@ struct FusedParams {
 // host side
 // ---------------------------------------------------------------------------
 inline int fused_ch(int d) { return (d / 8 + kGroup - 1) / kGroup; }
+// phase-4 partial-sum buffer (floats): [SPL][columns x B / 4][4] with SPL <= max(ceil(P / 8), 512 / items)
+__host__ __device__ constexpr int fused_spart(int P, int pcap, int B) {
+  return ((P + 7) / 8) * pcap * B > 4 * kConsumers ? ((P + 7) / 8) * pcap * B : 4 * kConsumers;
+}
 
 template <class Alloc>
 inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms, bool reglu, Alloc &&alloc,
@@ -159,14 +163,14 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   w.idcap = (m + w.P - 1) / w.P + 2;
   const int words_all = (m + 31) / 32;
   w.wcap = (words_all + w.P - 1) / w.P + 1;
-  w.pcap = (d + w.P - 1) / w.P + 1;
+  w.pcap = ((d / 8 + w.P - 1) / w.P + 1) * 8;   // phase-4 columns per CTA (8-column units), upper bound
   const int mb = std::max(1, std::min(maxB, kFusedMaxB));   // the kernel's B <= max_batch
   const int NT = (3 * mb + 7) / 8;
   // everything but the ring: mbarriers, reduction buffers, h, logits, b2, b_up/ids/bits, phase-4
   // partials, g staging and its B fragments; the ring gets the rest (<= 200 KB)
   auto extras = [&](int ns) {
     return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * mb * 4 +
-           (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)8 * w.pcap * mb * 4 +
+           (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)fused_spart(w.P, w.pcap, mb) * 4 +
            (size_t)mb * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
   };
   const size_t cap = 227 * 1024 - 2560;   // static shared memory (speculative tables, barriers) and slack
@@ -177,7 +181,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
                      (size_t)w.NS * 8 * mb * 4 + (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
   w.part_off = (int)(((size_t)w.NS * sb + pre + 15) / 16 * 16);
-  w.smem = w.part_off + 8 * w.pcap * mb * 4 + mb * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
+  w.smem = w.part_off + fused_spart(w.P, w.pcap, mb) * 4 + mb * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
   const int words = (m + 31) / 32;
   // a grouped workspace repeats every buffer per group with the strides of fused.cuh group_view
   const size_t G = (size_t)groups;
