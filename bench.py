@@ -54,6 +54,8 @@ def parse():
                     help="single-layer configs: CTAs per independent problem of the grouped launch (pi_group_run); "
                          "0 = the config default (c1: 2, c2: 8)")
     ap.add_argument("--group-layers", type=int, default=4, help="layer copies chained per group (grouped launch)")
+    ap.add_argument("--group-defer", type=int, default=0, choices=[0, 1, 2],
+                    help="grouped launch: 1/2 = PI_GROUP_DEFER_AFTER_REDUCTION/_BARRIER (pi_group_create flags)")
     ap.add_argument("--no-group", action="store_true",
                     help="single-layer configs: one pi_layer_forward per step over rotated copies instead of the "
                          "grouped launch")
@@ -408,7 +410,7 @@ def run_grouped(args, cfg, B, dev):
             st.stack.close()          # the group owns the launch
             st.stack = None
         stacks.append(st)
-    G = pi.GroupHandle([st.layers for st in stacks], pg)
+    G = pi.GroupHandle([st.layers for st in stacks], pg, flags=args.group_defer)
     d = cfg.d
     T = args.warmup + args.steps
     xs = torch.stack([torch.cat([gen.tokens(1, d, seed=args.seed + 7 + 31 * k, step=i, device=dev)[None]
@@ -471,6 +473,7 @@ def run_grouped(args, cfg, B, dev):
            "config": workload_config(cfg, B, 1, 1, {
                "realised_activity": round(realised, 4),
                "grouped": {"groups": ng, "ctas_per_group": pg, "layer_copies_per_group": gl,
+                           "flags": args.group_defer,
                            "layer_tokens_per_step": lt,
                            "note": "value = layer-tokens/s: each group decodes its own token through its own "
                                    "chain of distinct layer copies; all groups in one persistent launch"},

@@ -258,8 +258,14 @@ pi_status pi_stack_run_host(pi_stack *S, const float *x_host, int32_t B, float *
  * INVALID_ARGUMENT, SHAPE, UNSUPPORTED (no grouped kernel for the shape, e.g. r > 64 group_ctas),
  * OUT_OF_MEMORY, CUDA. */
 typedef struct pi_group pi_group;
+/* flags: 0, or one of PI_GROUP_DEFER_*: each group's weight producer requests a layer's predictor
+ * rows only after the group has finished the previous layer's reduction (AFTER_REDUCTION) or its
+ * last grid barrier (AFTER_BARRIER) instead of running ahead -- the group's barrier and reduction
+ * round trips then do not queue behind its own bulk loads while the other groups keep HBM busy. */
+#define PI_GROUP_DEFER_AFTER_REDUCTION 1u
+#define PI_GROUP_DEFER_AFTER_BARRIER 2u
 pi_status pi_group_create(pi_layer *const *layers, int32_t n_groups, int32_t n_layers, int32_t group_ctas,
-                          pi_group **out);
+                          uint32_t flags, pi_group **out);
 pi_status pi_group_destroy(pi_group *G);
 /* One step of every group: x, y dev fp32 [n_groups, B, d] (group k reads x[k], writes y[k]);
  * B must be 1; n_active_out: dev int32 [n_groups, n_layers] or NULL.  Graph capturable.

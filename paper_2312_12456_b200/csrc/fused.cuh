@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
   __shared__ float s_corr_h[SPEC ? kMaxCorrPerCta : 1][B];
   __shared__ int s_ncorr, s_count_full;
   __shared__ __align__(8) uint64_t s_b2_arrive, s_b2_done;   // SPEC: split-phase grid barrier 2
+  __shared__ __align__(8) uint64_t s_layer_done;   // defer_ring: the consumers finished layer l's tail
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[kMaxP1PerCta];
   __shared__ int s_n, s_k0, s_k1, s_count;
@@ -519,6 +520,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
     for (int s = 0; s < kMaxStages; ++s) s_slot_pos[s] = 0xffffffffu;
     mbar_init(&s_b2_arrive, 1);
     mbar_init(&s_b2_done, 1);
+    mbar_init(&s_layer_done, 1);
   }
   for (int i = tid; i < p.kt * 32; i += blockDim.x) gfrag[i] = make_uint2(0u, 0u);
   if (tid == 0) {
@@ -574,6 +576,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
     const size_t rowb2 = (size_t)p.kt * 16 * 2;   // bytes of one (padded) P2 row in the tiled layout
     for (int l = 0; l < L; ++l) {
       const LayerW lw = layer(l);
+      // defer_ring (grouped launches): layer l's predictor rows are requested only once the
+      // consumers have finished layer l-1's reduction (1) or its last grid barrier (2), so the
+      // group's barrier and reduction round trips do not queue behind this SM's bulk loads
+      if (p.defer_ring && l > 0) mbar_wait(&s_layer_done, (l - 1) & 1);
       if (l == (L > 1 ? 1 : 0)) trace_it0 = it;
       // The ring holds the layer's first NS predictor stages (issued while the previous layer
       // finished its FFN); stages >= NS can only be issued once the consumers free slots after
@@ -1274,7 +1280,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
       }
     }
     if (tr && tid == 0) tr[8] = globaltimer();
+    if (p.defer_ring == 1 && l < L - 1) {
+      consumers_sync();
+      if (tid == 0) mbar_arrive(&s_layer_done);
+    }
     if (l < L - 1) grid_sync(p.bar, P, tr ? tr + 216 : nullptr);   // the next layer reads all of y
+    if (p.defer_ring == 2 && l < L - 1 && tid == 0) mbar_arrive(&s_layer_done);
   }
 }
 

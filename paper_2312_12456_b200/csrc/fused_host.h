@@ -117,6 +117,8 @@ struct FusedParams {
   int rec_q4;                 // INT4 FFN records (bytes per neuron and matrix); 0 = 16-bit rows
   unsigned long long *trace;  // [P][256] timestamps (globaltimer ns) of layer 0, or NULL
   int hot_cap;                // at most this many hot neurons are L2-prefetched per layer
+  int defer_ring;             // 0: the producer runs ahead into the next layer; 1 / 2: it waits for the
+                              // previous layer's reduction / last grid barrier (pi_group_create flags)
   int group_ctas;             // > 0: grouped launch (pi_group_run) -- the grid is n_groups independent
                               // problems of group_ctas CTAs each; group k uses lws + k L, x/y + k B d and
                               // the k-th slice of every workspace buffer (strides: fused.cuh group_view)

@@ -534,6 +534,7 @@ extern "C" pi_status pi_stack_run_host(pi_stack *S, const float *x_host, int32_t
 struct pi_group {
   std::vector<pi_layer *> layers;   // [n_groups * n_layers], group-major
   int n_groups = 0, n_layers = 0, group_ctas = 0;
+  int defer = 0;                    // FusedParams.defer_ring from PI_GROUP_DEFER_*
   LayerW *lws = nullptr;            // device [n_groups * n_layers]
   FusedWork fw{};                   // geometry for P = group_ctas, buffers repeated per group
   std::vector<void *> allocs;
@@ -547,7 +548,7 @@ static void group_free(pi_group *G) {
 }
 
 extern "C" pi_status pi_group_create(pi_layer *const *layers, int32_t n_groups, int32_t n_layers,
-                                     int32_t group_ctas, pi_group **out) {
+                                     int32_t group_ctas, uint32_t flags, pi_group **out) {
   g_err.clear();
   if (!out) return fail(PI_ERR_INVALID_ARGUMENT, "group: out is NULL");
   *out = nullptr;
@@ -570,7 +571,11 @@ extern "C" pi_status pi_group_create(pi_layer *const *layers, int32_t n_groups, 
   if (group_ctas < 1 || (int64_t)group_ctas * n_groups > L0->num_sms)
     return fail(PI_ERR_INVALID_ARGUMENT, "group: n_groups %d x group_ctas %d exceeds the %d SMs", n_groups,
                 group_ctas, L0->num_sms);
+  if (flags & ~(uint32_t)(PI_GROUP_DEFER_AFTER_REDUCTION | PI_GROUP_DEFER_AFTER_BARRIER) ||
+      (flags & PI_GROUP_DEFER_AFTER_REDUCTION && flags & PI_GROUP_DEFER_AFTER_BARRIER))
+    return fail(PI_ERR_INVALID_ARGUMENT, "group: unknown or conflicting flags 0x%x", flags);
   pi_group *G = new pi_group();
+  G->defer = (flags & PI_GROUP_DEFER_AFTER_REDUCTION) ? 1 : (flags & PI_GROUP_DEFER_AFTER_BARRIER) ? 2 : 0;
   G->layers.assign(layers, layers + total);
   G->n_groups = n_groups;
   G->n_layers = n_layers;
@@ -647,6 +652,7 @@ extern "C" pi_status pi_group_run(pi_group *G, const float *x, int32_t B, float 
     p.ids_out = nullptr;
     p.trace = L0->fw.trace;      // pi_layer_set_trace on layer 0: group 0's CTAs stamp their phases
     p.group_ctas = G->group_ctas;
+    p.defer_ring = G->defer;
     cudaError_t e = fused_launch_p<T>(G->fw, p, a.reglu, B, (cudaStream_t)stream);
     if (e != cudaSuccess) return fail(PI_ERR_CUDA, "group: fused launch: %s", cudaGetErrorString(e));
     return PI_OK;

@@ -96,7 +96,7 @@ def _load() -> ctypes.CDLL:
     lib.pi_stack_destroy.argtypes = [vp]
     lib.pi_stack_run.argtypes = [vp, vp, i32, vp, vp, vp]
     lib.pi_stack_run_host.argtypes = [vp, vp, i32, vp, vp]
-    lib.pi_group_create.argtypes = [P(vp), i32, i32, i32, P(vp)]
+    lib.pi_group_create.argtypes = [P(vp), i32, i32, i32, ctypes.c_uint32, P(vp)]
     lib.pi_group_destroy.argtypes = [vp]
     lib.pi_group_run.argtypes = [vp, vp, i32, vp, vp, vp]
     dbl = ctypes.c_double
@@ -307,13 +307,13 @@ class GroupHandle:
     """Owns a pi_group: n_groups independent stacks of n_layers layers in ONE persistent launch,
     group_ctas CTAs per group (include/pi.h).  x, y: [n_groups, 1, d] device fp32."""
 
-    def __init__(self, groups: Sequence[Sequence[Layer]], group_ctas: int):
+    def __init__(self, groups: Sequence[Sequence[Layer]], group_ctas: int, flags: int = 0):
         self.layers = [L for g in groups for L in g]
         self.n_groups, self.n_layers = len(groups), len(groups[0])
         assert all(len(g) == self.n_layers for g in groups)
         arr = handles(self.layers)
         h = ctypes.c_void_p()
-        _check(_lib.pi_group_create(arr, self.n_groups, self.n_layers, group_ctas, ctypes.byref(h)))
+        _check(_lib.pi_group_create(arr, self.n_groups, self.n_layers, group_ctas, flags, ctypes.byref(h)))
         self.handle = h
         self.group_ctas = group_ctas
 
@@ -333,6 +333,8 @@ class GroupHandle:
             pass
 
 
+PI_GROUP_DEFER_AFTER_REDUCTION = 1
+PI_GROUP_DEFER_AFTER_BARRIER = 2
 pi_group_create = GroupHandle
 pi_group_run = GroupHandle.run
 pi_stack_create = StackHandle

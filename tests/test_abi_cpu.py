@@ -144,7 +144,7 @@ def test_null_handles(pi):
     assert lib.pi_stack_run(None, None, 1, None, None, None) == 1
     assert lib.pi_stack_run_host(None, None, 1, None, None) == 1
     assert "NULL" in lib.pi_last_error().decode()
-    assert lib.pi_group_create(None, 1, 1, 1, None) == 1
+    assert lib.pi_group_create(None, 1, 1, 1, 0, None) == 1
     assert lib.pi_group_destroy(None) == 0
     assert lib.pi_group_run(None, None, 1, None, None, None) == 1
     assert "NULL" in lib.pi_last_error().decode()

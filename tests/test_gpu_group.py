@@ -80,8 +80,9 @@ def test_group_random_full_size_vs_oracle(env, name, pg):
     G.close()
 
 
+@pytest.mark.parametrize("flags", [0, 1, 2])
 @pytest.mark.parametrize("name,dims,pg", [("c1", None, 2), ("c2", None, 8), ("c4", (8192, 4096, 512), 16)])
-def test_group_chain_equals_stack(env, name, dims, pg):
+def test_group_chain_equals_stack(env, name, dims, pg, flags):
     """Groups of 3 chained layers: each group's output equals the same layers run as an ordinary
     stack on all SMs (pi_stack_run) to fp32 summation order, and the layer-0 union counts agree."""
     gen, pi = env
@@ -90,7 +91,7 @@ def test_group_chain_equals_stack(env, name, dims, pg):
     dd = {} if dims is None else dict(d=dims[0], m=dims[1], r=dims[2])
     ng, gl = 3, 3
     stacks = [build_stack(cfg, n_layers=gl, seed=100 * k, device="cuda", max_batch=1, dims=dd)[0] for k in range(ng)]
-    G = pi.GroupHandle([st.layers for st in stacks], pg)
+    G = pi.GroupHandle([st.layers for st in stacks], pg, flags=flags)   # flags: PI_GROUP_DEFER_* (0: none)
     d = stacks[0].d
     x = torch.stack([gen.tokens(1, d, seed=k, device="cuda") for k in range(ng)])
     y = torch.empty(ng, 1, d, device="cuda")
@@ -118,6 +119,8 @@ def test_group_validation(env):
     L = pi.Layer(w, max_batch=2)
     with pytest.raises(pi.PiError):
         pi.GroupHandle([[L]] * 2, 100)          # 2 x 100 CTAs > SMs
+    with pytest.raises(pi.PiError):
+        pi.GroupHandle([[L]], 2, flags=3)       # conflicting PI_GROUP_DEFER_* flags
     G = pi.GroupHandle([[L]], 2)
     x = torch.zeros(1, 2, 256, device="cuda")
     y = torch.zeros(1, 2, 256, device="cuda")
