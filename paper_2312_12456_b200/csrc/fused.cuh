@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
   __shared__ float s_ss[kGroupWarps][B];
   __shared__ float s_b1[kMaxP1PerCta];
   __shared__ int s_n, s_k0, s_k1, s_count;
+  __shared__ const uint32_t *s_hot_words;   // this layer's hot bitmap (hot-first FFN order) or NULL
   unsigned long long *trace = p.trace ? p.trace + (size_t)c * 256 : nullptr;
   if (trace && tid == 0) trace[0] = globaltimer();
 
@@ -611,6 +612,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
         // would cost an HBM round trip at the start of the layer: pull them into L2 now
         const uint64_t keep = policy_evict_last();
         if (lw.p_b1 && c == 0) prefetch_l2(lw.p_b1, (uint32_t)(((size_t)r * 2 + 15) & ~(size_t)15), keep);
+        // the hot bitmap every CTA stages in its compaction (hot-first FFN order)
+        if (lw.hot_words && lw.n_hot > 0 && c == 1 % P)
+          prefetch_l2(lw.hot_words, (uint32_t)(((size_t)p.words * 4 + 15) & ~(size_t)15), keep);
         if (lw.p_b2) {
           const size_t a0 = ((size_t)w0 * 64) & ~(size_t)15;
           const size_t a1 = min((size_t)m * 2 & ~(size_t)15, ((size_t)min(m, w1 * 32) * 2 + 15) & ~(size_t)15);
@@ -723,6 +727,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
       s_count = 0;
       s_count_full = 0;
       s_ncorr = 0;
+      s_hot_words = lw.n_hot > 0 ? lw.hot_words : nullptr;
     }
     if (tid < B) s_gmax[tid] = 0u;
     if (tr && tid == 0) tr[0] = globaltimer();
@@ -939,15 +944,52 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
     uint32_t *c_msk = c_uni + p.words;                                   // [B][words] (stage_tok)
     int *c_cnt = reinterpret_cast<int *>(c_msk + (stage_tok ? B * p.words : 0));   // [P]
     int *c_cntf = c_cnt + P;                                              // [P] (SPEC)
-    for (int i = tid; i < p.words; i += kConsumers) {
-      c_uni[i] = __ldcg(p.uni + i);
-      if (stage_tok)
+    // hot-first FFN order: each CTA streams its share's prefetched hot neurons (L2 hits) first
+    // (the bitmap pointer was staged at the layer start: reading it from the layer table here
+    // would put a dependent L2 round trip on the compaction's critical path)
+    const uint32_t *hot_words = s_hot_words;
+    const bool hot_on = !SPEC && hot_words != nullptr;
+    uint32_t *c_hot = reinterpret_cast<uint32_t *>(c_cntf + P);         // [words] (hot_on)
+    {
+      // every load of the staging first, then the shared stores: one L2 round trip (a store to
+      // the generic ring pointer between loads would order each load after the previous store)
+      constexpr int WPT = 4;                                              // words per thread
+      uint32_t vu[WPT], vh[WPT], vm[WPT][B];
+      int vc = 0, vcf = 0;
 #pragma unroll
-        for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
-    }
-    if (tid < P) {
-      c_cnt[tid] = __ldcg(p.counts + tid);
-      if (SPEC && spec_on) c_cntf[tid] = __ldcg(p.counts_full + tid);
+      for (int q = 0; q < WPT; ++q) {
+        const int i = tid + q * kConsumers;
+        const bool ok = i < p.words;
+        vu[q] = ok ? __ldcg(p.uni + i) : 0u;
+        vh[q] = (ok && hot_on) ? __ldg(hot_words + i) : 0u;
+#pragma unroll
+        for (int b = 0; b < B; ++b) vm[q][b] = (ok && stage_tok) ? __ldcg(p.mask + (size_t)b * p.words + i) : 0u;
+      }
+      if (tid < P) {
+        vc = __ldcg(p.counts + tid);
+        if (SPEC && spec_on) vcf = __ldcg(p.counts_full + tid);
+      }
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) {
+        const int i = tid + q * kConsumers;
+        if (i < p.words) {
+          c_uni[i] = vu[q];
+          if (hot_on) c_hot[i] = vh[q];
+          if (stage_tok)
+#pragma unroll
+            for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = vm[q][b];
+        }
+      }
+      if (tid < P) {
+        c_cnt[tid] = vc;
+        if (SPEC && spec_on) c_cntf[tid] = vcf;
+      }
+      for (int i = tid + WPT * kConsumers; i < p.words; i += kConsumers) {   // m > 65536 only
+        c_uni[i] = __ldcg(p.uni + i);
+        if (hot_on) c_hot[i] = __ldg(hot_words + i);
+        if (stage_tok)
+          for (int b = 0; b < B; ++b) c_msk[b * p.words + i] = __ldcg(p.mask + (size_t)b * p.words + i);
+      }
     }
     consumers_sync();
     if (warp == 0) {
@@ -1030,6 +1072,43 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
         s_k0 = k0;
         s_k1 = k1;
       }
+      if (hot_on) {
+        // stable partition of the share [k0, k1): hot neurons first (ascending), then the rest
+        // (ascending) -- a fixed order given the mask.  ids_out keeps the ascending order.
+        __syncwarp();
+        const int nm = k1 - k0;
+        int *tmp = reinterpret_cast<int *>(s_bup);   // free until the b_up gather below
+        int nh = 0;
+        for (int base = 0; base < nm; base += 32) {
+          const int k = base + lane;
+          bool hot = false;
+          if (k < nm) {
+            const int id = s_ids[k];
+            tmp[k] = id | ((int)s_bits[k] << 24);
+            hot = (c_hot[id >> 5] >> (id & 31)) & 1u;
+            if (p.ids_out) p.ids_out[k0 + k] = id;
+          }
+          nh += __popc(__ballot_sync(0xffffffffu, hot));
+        }
+        __syncwarp();
+        int ph = 0, pc = nh;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (int base = 0; base < nm; base += 32) {
+          const int k = base + lane;
+          const bool ok = k < nm;
+          const int v = ok ? tmp[k] : 0;
+          const int id = v & 0xFFFFFF;
+          const bool hot = ok && ((c_hot[id >> 5] >> (id & 31)) & 1u);
+          const uint32_t bh = __ballot_sync(0xffffffffu, hot), bc = __ballot_sync(0xffffffffu, ok && !hot);
+          if (ok) {
+            const int dst = hot ? ph + __popc(bh & lt) : pc + __popc(bc & lt);
+            s_ids[dst] = id;
+            s_bits[dst] = (uint8_t)((unsigned)v >> 24);
+          }
+          ph += __popc(bh);
+          pc += __popc(bc);
+        }
+      }
     } else if (SPEC && warp == 1) {
       // corrections: my speculative neurons whose bit is 0 for some token (ascending k, fixed order)
       int nc = 0;
@@ -1063,7 +1142,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
     for (int k = tid; k < n_mine; k += kConsumers) {
       const int i = s_ids[k];
       s_bup[k] = lw.b_up ? WT<T>::to_float(lw.b_up, i) : 0.f;
-      if (p.ids_out) p.ids_out[k0 + k] = i;
+      if (p.ids_out && !hot_on) p.ids_out[k0 + k] = i;
     }
     if (p.n_out && c == 0 && tid == 0) p.n_out[l] = s_n;
     consumers_sync();

@@ -81,6 +81,7 @@ struct FusedArgs {
   uint32_t *mask_out;
   int32_t *ids_out, *n_out;
   const int32_t *hot_ids;
+  const uint32_t *hot_words;
   int n_hot, hot_cap;
   bool spec;   // stack launch whose layers carry speculative tables
 };
@@ -89,6 +90,7 @@ struct LayerW {  // one layer's library-owned weights (device pointers)
   const uint8_t *w_up, *w_down, *p_w1, *p_w2;
   const void *b_up, *b_down, *p_b1, *p_b2;
   const int32_t *hot_ids;   // local ids of the hot neurons (L2-prefetched each step), or NULL
+  const uint32_t *hot_words;  // [words] bitmap of the prefetched hot neurons (FFN order: hot first), or NULL
   int n_hot;
   float t;
   const int32_t *spec_ids;      // speculative hot prefix (hottest first), or NULL
@@ -158,8 +160,8 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   while (na < 8 && 2 * na * nb <= (size_t)(rec_q4 ? 48 : 40) * 1024) na *= 2;
   size_t sb = std::max<size_t>({(size_t)32 * 1024, na * nb, p2_word});
   sb = (sb + 127) / 128 * 128;
-  // compaction stages the union words, the per-token words and the P counts in one ring slot
-  if ((size_t)((m + 31) / 32) * (1 + kFusedMaxB) * 4 + (size_t)2 * num_sms * 4 > sb) return true;
+  // compaction stages the union words, the per-token words, the hot bitmap and the P counts in one ring slot
+  if ((size_t)((m + 31) / 32) * (2 + kFusedMaxB) * 4 + (size_t)2 * num_sms * 4 > sb) return true;
   w.stage_bytes = (int)sb;
   w.words_p2 = std::min<int>(kMaxWordsP2, (int)(sb / p2_word));
   w.idcap = (m + w.P - 1) / w.P + 2;
@@ -267,6 +269,7 @@ inline FusedParams fused_params(const FusedWork &w, const FusedArgs &a) {
   p.lw0.p_b2 = a.p_b2;
   p.lw0.t = a.threshold;
   p.lw0.hot_ids = a.hot_ids;
+  p.lw0.hot_words = a.hot_words;
   p.lw0.n_hot = a.n_hot;
   p.lws = nullptr;
   p.L = 1;

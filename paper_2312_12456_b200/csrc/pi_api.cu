@@ -88,6 +88,7 @@ struct pi_layer {
   unsigned *tickets_tc = nullptr;
   int S_tc = 0;
   int32_t *hot_ids = nullptr;              // [n_hot] local ids of hot neurons, hottest first
+  uint32_t *hot_words = nullptr;           // [words] bitmap of the first hot_cap of them (prefetched set)
   int n_hot = 0, hot_cap = 0;
   int32_t *spec_ids = nullptr;             // [n_spec] speculative hot prefix, hottest first
   uint32_t *spec_words = nullptr;          // [words] bitmap of the speculative neurons
@@ -334,6 +335,12 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
       if (cudaMemcpy(L->hot_ids, hot.data(), hot.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
         return cleanup(fail(PI_ERR_CUDA, "layer %d: hot table copy", lid));
       L->n_hot = (int)hot.size();
+      std::vector<uint32_t> hw(L->words, 0u);
+      for (int k = 0; k < std::min((int)hot.size(), L->hot_cap); ++k) hw[hot[k] >> 5] |= 1u << (hot[k] & 31);
+      st = dev_alloc(L, (void **)&L->hot_words, hw.size() * 4, false);
+      if (st != PI_OK) return cleanup(st);
+      if (cudaMemcpy(L->hot_words, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        return cleanup(fail(PI_ERR_CUDA, "layer %d: hot bitmap copy", lid));
     }
   }
   int32_t *d_nid = nullptr;
@@ -453,6 +460,7 @@ extern "C" pi_status pi_stack_create(pi_layer *const *layers, int32_t n_layers, 
     h[l].p_b2 = Ll->p_b2;
     h[l].t = Ll->threshold;
     h[l].hot_ids = Ll->hot_ids;
+    h[l].hot_words = Ll->hot_words;
     h[l].n_hot = std::min(Ll->n_hot, Ll->hot_cap);
     h[l].spec_ids = Ll->spec_ids;
     h[l].spec_words = Ll->spec_words;
@@ -609,6 +617,7 @@ extern "C" pi_status pi_group_create(pi_layer *const *layers, int32_t n_groups, 
     h[i].p_b2 = Ll->p_b2;
     h[i].t = Ll->threshold;
     h[i].hot_ids = Ll->hot_ids;
+    h[i].hot_words = Ll->hot_words;
     h[i].n_hot = std::min(Ll->n_hot, Ll->hot_cap);
   }
   if (cudaMalloc(&G->lws, sizeof(LayerW) * total) != cudaSuccess ||
@@ -786,7 +795,7 @@ static pi_status forward_dev(pi_layer *L, const float *x, int B, float *y, uint3
       a.threshold = L->threshold; a.rmsnorm = (L->flags & PI_FLAG_INPUT_RMSNORM) != 0;
       a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
       a.mask_out = mask_out; a.ids_out = ids_out; a.n_out = n_out;
-      a.hot_ids = L->hot_ids; a.n_hot = L->n_hot; a.hot_cap = L->hot_cap;
+      a.hot_ids = L->hot_ids; a.hot_words = L->hot_words; a.n_hot = L->n_hot; a.hot_cap = L->hot_cap;
       cudaError_t e = fused_launch<T>(L->fw, a, L->num_sms, s);
       if (e != cudaSuccess) return fail(PI_ERR_CUDA, "layer %d: fused launch: %s", L->layer_id, cudaGetErrorString(e));
       return PI_OK;
