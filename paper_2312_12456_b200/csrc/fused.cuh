@@ -301,6 +301,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
     const uint8_t *a_base = x.stages + (size_t)slot * x.SB + (size_t)(2 * (jj >> 2) + rt) * kt * kP2Tile + lane * 16;
     const uint2 *b_base = x.gfrag + lane;
     int K = k0;
+#pragma unroll 4
     for (; K + 1 < k1; K += 2) {
       const uint4 a0 = *reinterpret_cast<const uint4 *>(a_base + (size_t)K * kP2Tile);
       const uint4 a1 = *reinterpret_cast<const uint4 *>(a_base + (size_t)(K + 1) * kP2Tile);

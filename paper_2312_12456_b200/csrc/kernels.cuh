@@ -265,20 +265,47 @@ __global__ void __launch_bounds__(256) k_down(const T *__restrict__ wdt, const T
   for (int b = 0; b < B; ++b)
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[b][q] = 0.f;
-  if (valid) {
-#pragma unroll 4
-    for (int k = k0 + warp; k < k1; k += 8) {
-      const int i = ids[k];
-      float wf[8];
-      WT<T>::unpack(ld_stream(wdt + (int64_t)i * d + col), wf);
+  // The split's ids and h are staged through shared memory 256 rows at a time (one coalesced
+  // round trip), so each warp's weight loads -- 8 rows in flight -- depend on nothing global.
+  // Warp w still walks rows k0 + w, k0 + w + 8, ... in ascending order (same sums as before).
+  int *s_id = reinterpret_cast<int *>(red);   // [256]      (aliases red until the reduction)
+  float *s_h = red + 256;                     // [B][256]
+  for (int base = k0; base < k1; base += 256) {
+    const int nc = min(256, k1 - base);
+    __syncthreads();                          // the previous chunk has been consumed
+    if ((int)threadIdx.x < nc) {
+      s_id[threadIdx.x] = ids[base + threadIdx.x];
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const float hb = h[(int64_t)b * hstride + k];
+      for (int b = 0; b < B; ++b) s_h[b * 256 + threadIdx.x] = h[(int64_t)b * hstride + base + threadIdx.x];
+    }
+    __syncthreads();
+    if (valid) {
+      for (int r0 = warp; r0 < nc; r0 += 64) {
+        Pack8 wv[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[b][q] = fmaf(hb, wf[q], acc[b][q]);
+        for (int j = 0; j < 8; ++j) {
+          const int r = r0 + 8 * j;
+          if (r < nc) wv[j] = ld_stream(wdt + (int64_t)s_id[r] * d + col);
+          else wv[j].u[0] = wv[j].u[1] = wv[j].u[2] = wv[j].u[3] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = r0 + 8 * j;
+          if (r < nc) {
+            float wf[8];
+            WT<T>::unpack(wv[j], wf);
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+              const float hb = s_h[b * 256 + r];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[b][q] = fmaf(hb, wf[q], acc[b][q]);
+            }
+          }
+        }
       }
     }
   }
+  __syncthreads();                            // staging done before red is written
 #pragma unroll
   for (int b = 0; b < B; ++b)
 #pragma unroll
