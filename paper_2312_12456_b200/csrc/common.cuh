@@ -205,4 +205,31 @@ __device__ __forceinline__ void ld_x8(const float *p, float (&f)[8]) {
   f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
 }
 
+// Transpose reduction of NV per-lane partials (NV a power of two <= 32): afterwards every
+// lane l holds the warp-wide total of value (l & (NV - 1)).  NV - 1 + log2(32 / NV) shuffles
+// instead of 5 NV.  Fixed order.
+template <int NV>
+__device__ __forceinline__ float warp_reduce_multi(float (&v)[NV]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = NV / 2; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const float send = up ? v[i] : v[i + s];
+      const float keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (int o = NV; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
+template <int N>
+struct Pow2Ceil {
+  static constexpr int v = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
+};
+
 }  // namespace pi

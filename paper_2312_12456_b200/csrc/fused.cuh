@@ -127,33 +127,6 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar, int P, unsign
   consumers_sync();
 }
 
-// Transpose reduction of NV per-lane partials (NV a power of two <= 32): afterwards every
-// lane l holds the warp-wide total of value (l & (NV - 1)).  NV - 1 + log2(32 / NV) shuffles
-// instead of 5 NV.  Fixed order.
-template <int NV>
-__device__ __forceinline__ float warp_reduce_multi(float (&v)[NV]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int s = NV / 2; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const float send = up ? v[i] : v[i + s];
-      const float keep = up ? v[i + s] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  float r = v[0];
-#pragma unroll
-  for (int o = NV; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-  return r;
-}
-
-template <int N>
-struct Pow2Ceil {
-  static constexpr int v = N <= 1 ? 1 : N <= 2 ? 2 : N <= 4 ? 4 : N <= 8 ? 8 : N <= 16 ? 16 : 32;
-};
-
 // Up-group reduction of NV values (NV <= 32): per-warp transpose reduction, lanes < NV write
 // red[warp][l]; after the 256-thread barrier, red holds 8 partials per value.
 template <int NV>
@@ -675,14 +648,22 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
       }
       mbar_wait(ids_ready, l & 1);                 // phase 3: after the ids are published
       const int n_mine = s_k1 - s_k0;
+      const uint8_t *wup = lw.w_up, *wdn = lw.w_down;
       for (int k0 = 0; k0 < n_mine; k0 += G, ++it) {
         const int kn = min(G, n_mine - k0);
+        // the stage's ids first (the copies' "memory" clobbers would order each id read after
+        // the previous copy): no shared-memory round trip between consecutive copies
+        int sid[NA];
+#pragma unroll
+        for (int k = 0; k < NA; ++k) sid[k] = (k < kn) ? s_ids[k0 + k] : 0;
         uint8_t *dst = acquire((uint32_t)(kn * nb));
         const int s = it % NS;
-        for (int k = 0; k < kn; ++k) {
-          const int i = s_ids[k0 + k];
-          bulk_g2s(dst + (size_t)k * nb, lw.w_up + (size_t)i * row_up, (uint32_t)row_up, &full[s], pol);
-          bulk_g2s(dst + (size_t)k * nb + row_up, lw.w_down + (size_t)i * row_dn, (uint32_t)row_dn, &full[s], pol);
+#pragma unroll
+        for (int k = 0; k < NA; ++k) {
+          if (k < kn) {
+            bulk_g2s(dst + (size_t)k * nb, wup + (size_t)sid[k] * row_up, (uint32_t)row_up, &full[s], pol);
+            bulk_g2s(dst + (size_t)k * nb + row_up, wdn + (size_t)sid[k] * row_dn, (uint32_t)row_dn, &full[s], pol);
+          }
         }
       }
       if constexpr (SPEC) {

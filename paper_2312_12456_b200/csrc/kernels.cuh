@@ -238,6 +238,104 @@ __global__ void __launch_bounds__(256) k_up(const T *__restrict__ wup, const T *
 }
 
 // ---------------------------------------------------------------------------
+// a4 for 6 <= B <= 8 (x-stationary): a warp owns one 256-column slice of d and keeps those
+// columns of x in registers for all B tokens (8 per lane); it walks a range of compacted rows,
+// 4 rows' (gate and) up loads in flight, and writes each row's per-slice dot products (transpose
+// reduction, one 64-byte store) to upart[slice][k][2][B].  k_up_fin then sums the slices in
+// ascending order and applies the scale, b_up, the activation and the token's bit.  Replaces the
+// warp-per-row k_up for these batches, which re-read all of x (B x d x 4 bytes) for every row.
+// ---------------------------------------------------------------------------
+template <typename T, int B, bool REGLU>
+__global__ void __launch_bounds__(256) k_up_xs(const T *__restrict__ wup, const float *__restrict__ x,
+                                                const int32_t *__restrict__ ids,
+                                                const int32_t *__restrict__ n_active, int d, int m,
+                                                float *__restrict__ upart) {
+  constexpr int NV = (REGLU ? 2 : 1) * B;      // values per row: [gate | up] x tokens
+  constexpr int NP = Pow2Ceil<NV>::v;
+  constexpr int RU = 4;                        // rows in flight per warp
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int KW = (d + 255) / 256;              // 256-column slices
+  const int R = max(1, nw / KW);               // row ranges per slice
+  const int kt = gw % KW, rp = gw / KW;
+  if (rp >= R) return;
+  const int n = *n_active;
+  const int r0 = (int)(((int64_t)rp * n) / R), r1 = (int)(((int64_t)(rp + 1) * n) / R);
+  const int col = kt * 256 + lane * 8;
+  const bool valid = col < d;
+  const int64_t rowlen = REGLU ? 2 * (int64_t)d : (int64_t)d;
+  float xr[B][8];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    if (valid) ld_x8(x + (int64_t)b * d + col, xr[b]);
+    else
+#pragma unroll
+      for (int e = 0; e < 8; ++e) xr[b][e] = 0.f;
+  }
+  for (int r = r0; r < r1; r += RU) {
+    Pack8 wu[RU], wg[RU];
+#pragma unroll
+    for (int j = 0; j < RU; ++j) {
+      const bool ok = valid && r + j < r1;
+      const T *row = wup + (int64_t)(ok ? ids[r + j] : 0) * rowlen;
+      if (ok) {
+        wu[j] = ld_stream(row + (REGLU ? d : 0) + col);
+        if (REGLU) wg[j] = ld_stream(row + col);
+      } else {
+        wu[j].u[0] = wu[j].u[1] = wu[j].u[2] = wu[j].u[3] = 0u;
+        wg[j] = wu[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RU; ++j) {
+      if (r + j >= r1) break;
+      float acc[NP];
+#pragma unroll
+      for (int v = 0; v < NP; ++v) acc[v] = 0.f;
+      float fu[8], fg[8];
+      WT<T>::unpack(wu[j], fu);
+      if (REGLU) WT<T>::unpack(wg[j], fg);
+#pragma unroll
+      for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (REGLU) acc[b] = fmaf(fg[e], xr[b][e], acc[b]);
+          acc[(REGLU ? B : 0) + b] = fmaf(fu[e], xr[b][e], acc[(REGLU ? B : 0) + b]);
+        }
+      const float tot = warp_reduce_multi<NP>(acc);   // lane l: total of value l & (NP - 1)
+      if (lane < NV) upart[((int64_t)kt * m + r + j) * (2 * B) + (REGLU ? 0 : B) + lane] = tot;
+    }
+  }
+}
+
+// h[b, k] = masked act(s_b * up + b_up) from the slice partials (ascending slice order)
+template <typename T, int B, bool REGLU>
+__global__ void __launch_bounds__(256) k_up_fin(const float *__restrict__ upart, const T *__restrict__ bup,
+                                                 const float *__restrict__ scale, const int32_t *__restrict__ ids,
+                                                 const int32_t *__restrict__ n_active,
+                                                 const uint32_t *__restrict__ mask, int words, int d, int m,
+                                                 float *__restrict__ h, int hstride) {
+  const int n = *n_active;
+  const int KW = (d + 255) / 256;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n * B; t += gridDim.x * blockDim.x) {
+    const int k = t / B, b = t - k * B;
+    float a = 0.f, g = 0.f;
+    for (int kt = 0; kt < KW; ++kt) {
+      const float *pp = upart + ((int64_t)kt * m + k) * (2 * B);
+      a += __ldcg(pp + B + b);
+      if (REGLU) g += __ldcg(pp + b);
+    }
+    const int i = ids[k];
+    const float s = scale ? scale[b] : 1.f;
+    a = a * s + (bup ? WT<T>::to_float(bup, i) : 0.f);
+    float hv = REGLU ? fmaxf(g * s, 0.f) * a : fmaxf(a, 0.f);
+    if (mask && !((mask[(int64_t)b * words + (i >> 5)] >> (i & 31)) & 1u)) hv = 0.f;
+    h[(int64_t)b * hstride + k] = hv;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // a5: column-sparse down GEMV, y_b = b_down + sum_k h[b,k] Wd_T[ids[k], :].
 // Block (tile, split): 8 warps own a 256-column tile; split s walks compacted
 // positions [s n / S, (s+1) n / S).  Warps reduce in fixed order through shared
@@ -626,12 +724,31 @@ cudaError_t steps_ffn(const StepArgs &a, const float *x, int B, const float *sca
                                                          a.tickets, y);
       return cudaGetLastError();
     }
-    if (a.reglu)
-      k_up<T, NB, true><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
-                                            a.words, a.d, a.h, a.m);
-    else
-      k_up<T, NB, false><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
-                                             a.words, a.d, a.h, a.m);
+    bool xs = false;
+    if constexpr (NB >= 6) {   // measured (c3): B = 8 5.73 -> 5.06 ms/token; B = 4 3.49 -> 3.66 (k_up kept)
+      if (a.upart) {   // x-stationary up projection + slice reduction
+        xs = true;
+        const int gxs = a.num_sms * 8;   // 64 warps per SM
+        const int gfin = std::max(1, std::min((a.m * NB + 255) / 256, a.num_sms * 4));
+        if (a.reglu) {
+          k_up_xs<T, NB, true><<<gxs, 256, 0, s>>>((const T *)a.w_up, x, ids, n_active, a.d, a.m, a.upart);
+          k_up_fin<T, NB, true><<<gfin, 256, 0, s>>>(a.upart, (const T *)a.b_up, scale, ids, n_active, mask,
+                                                     a.words, a.d, a.m, a.h, a.m);
+        } else {
+          k_up_xs<T, NB, false><<<gxs, 256, 0, s>>>((const T *)a.w_up, x, ids, n_active, a.d, a.m, a.upart);
+          k_up_fin<T, NB, false><<<gfin, 256, 0, s>>>(a.upart, (const T *)a.b_up, scale, ids, n_active, mask,
+                                                      a.words, a.d, a.m, a.h, a.m);
+        }
+      }
+    }
+    if (!xs) {
+      if (a.reglu)
+        k_up<T, NB, true><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
+                                              a.words, a.d, a.h, a.m);
+      else
+        k_up<T, NB, false><<<gup, 256, 0, s>>>((const T *)a.w_up, (const T *)a.b_up, x, scale, ids, n_active, mask,
+                                               a.words, a.d, a.h, a.m);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)8 * NB * 256 * 4;

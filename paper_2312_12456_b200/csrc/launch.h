@@ -13,6 +13,7 @@ namespace pi {
 struct StepArgs {
   const void *p_w1, *p_b1, *p_w2, *p_b2, *w_up, *b_up, *w_down, *b_down;
   float *g, *h, *partial;
+  float *upart;       // [ceil(d/256)][m][2][B] slice partials of k_up_xs (6 <= B <= 8), or NULL
   unsigned *tickets;
   int d, m, r, kt, words, S, tiles, num_sms;
   float t;

@@ -76,6 +76,7 @@ struct pi_layer {
   float *scale = nullptr;     // [max_batch]
   float *h = nullptr;         // [max_batch, m_local]
   float *partial = nullptr;   // [S, max_batch, d]
+  float *upart = nullptr;     // [ceil(d/256), m_local, 2, min(max_batch, 8)] (k_up_xs, max_batch >= 6)
   unsigned *tickets = nullptr;  // [tiles]
   uint32_t *mask = nullptr;   // [max_batch, words]
   int32_t *ids = nullptr;     // [m_local]
@@ -272,6 +273,7 @@ extern "C" pi_status pi_layer_create(const pi_layer_desc *D, pi_stream_t stream,
   ALLOC(L->scale, (size_t)MB * 4, false);
   ALLOC(L->h, (size_t)MB * ml * 4, false);
   ALLOC(L->partial, (size_t)L->S * MB * d * 4, false);
+  if (MB >= 6 && !q4) ALLOC(L->upart, (size_t)((d + 255) / 256) * ml * 2 * std::min(MB, 8) * 4, false);
   ALLOC(L->tickets, (size_t)L->tiles * 4, false);
   ALLOC(L->mask, (size_t)MB * L->words * 4, false);
   ALLOC(L->ids, (size_t)ml * 4, false);
@@ -717,7 +719,7 @@ static StepArgs step_args(const pi_layer *L) {
   StepArgs a{};
   a.p_w1 = L->p_w1; a.p_b1 = L->p_b1; a.p_w2 = L->p_w2; a.p_b2 = L->p_b2;
   a.w_up = L->w_up; a.b_up = L->b_up; a.w_down = L->w_down; a.b_down = L->b_down;
-  a.g = L->g; a.h = L->h; a.partial = L->partial; a.tickets = L->tickets;
+  a.g = L->g; a.h = L->h; a.partial = L->partial; a.tickets = L->tickets; a.upart = L->upart;
   a.d = L->d; a.m = L->m_local; a.r = L->r; a.kt = (L->r + 15) / 16; a.words = L->words; a.S = L->S; a.tiles = L->tiles;
   a.num_sms = L->num_sms; a.t = L->threshold;
   a.pred_relu = L->pred_act == PI_PRED_RELU; a.reglu = L->act == PI_ACT_REGLU;
