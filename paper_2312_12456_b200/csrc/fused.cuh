@@ -352,6 +352,21 @@ __device__ __forceinline__ auto &pick(A &a, Bb &b) {
   else return b;
 }
 
+// x chunk ch (8 consecutive columns) of all B tokens from the shared-memory copy (zeros past d)
+template <int B>
+__device__ __forceinline__ void load_x8(const float *s_x, int d, int ch, bool ok, float (&xq)[8][B]) {
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+    if (ok) {
+      a0 = reinterpret_cast<const float4 *>(s_x + (size_t)b * d + ch * 8)[0];
+      a1 = reinterpret_cast<const float4 *>(s_x + (size_t)b * d + ch * 8)[1];
+    }
+    xq[0][b] = a0.x; xq[1][b] = a0.y; xq[2][b] = a0.z; xq[3][b] = a0.w;
+    xq[4][b] = a1.x; xq[5][b] = a1.y; xq[6][b] = a1.z; xq[7][b] = a1.w;
+  }
+}
+
 // this CTA's partial y (register-resident, down group) -> global [B][d]
 template <int B, int CH>
 __device__ __forceinline__ void store_partial(const float (&yr)[CH][8][B], float *dst0, int d, int gt, int chunks) {
@@ -422,6 +437,7 @@ __device__ __forceinline__ FusedParams group_view(const FusedParams &a, int k, i
 template <typename T, int B, bool REGLU, int CH, int NA, bool SPEC, bool Q4, bool GRP = false>
 __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0) {
   constexpr int RPM = fused_rpm(CH);          // max P1 rows per stage (fused_geometry)
+  constexpr bool XS = B >= 2;                  // x staged in shared memory (fused_alloc: s_x)
   extern __shared__ __align__(128) uint8_t fsmem[];
   uint8_t *smem = fsmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -449,6 +465,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
   float *s_part = reinterpret_cast<float *>(fsmem + p.part_off);     // phase-4 partial sums (fused_spart)
   float *sg = s_part + fused_spart(P, p.pcap, B);                    // [B][kt*16] staging of g
   uint2 *gfrag = reinterpret_cast<uint2 *>(sg + B * p.kt * 16);       // [kt][NT][32] B fragments
+  float *s_x = reinterpret_cast<float *>(gfrag + p.kt * ((3 * B + 7) / 8) * 32);   // [B][d] (XS)
   __shared__ unsigned s_gmax[B];
   __shared__ uint32_t s_slot_pos[kMaxStages];
   // SPEC: this CTA's share of the speculative hot prefix and its corrections
@@ -724,33 +741,43 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
       }
     }
 
-    float xr[CH][8][B];   // up group: x chunks (live for the whole layer)
+    // up group: x chunks, in registers for the whole layer (B = 1), or -- B = 2, where registers
+    // for x and the down group's y spill at the 96-register cap -- in shared memory (s_x [B][d]),
+    // re-read per stage (each thread reads back only the chunks it wrote)
+    float xr[XS ? 1 : CH][8][B];
     float sc[B];
     if (is_up) {
+      float ssl[B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) ssl[b] = 0.f;
 #pragma unroll
       for (int q = 0; q < CH; ++q) {
         const int ch = gt + q * kGroup;
 #pragma unroll
         for (int b = 0; b < B; ++b) {
+          float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
           if (ch < chunks) {
-            const float4 a0 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8));
-            const float4 a1 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8) + 1);
-            xr[q][0][b] = a0.x; xr[q][1][b] = a0.y; xr[q][2][b] = a0.z; xr[q][3][b] = a0.w;
-            xr[q][4][b] = a1.x; xr[q][5][b] = a1.y; xr[q][6][b] = a1.z; xr[q][7][b] = a1.w;
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) xr[q][k][b] = 0.f;
+            a0 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8));
+            a1 = __ldcg(reinterpret_cast<const float4 *>(xin + (size_t)b * d + ch * 8) + 1);
           }
+          if constexpr (XS) {
+            if (ch < chunks) {
+              reinterpret_cast<float4 *>(s_x + (size_t)b * d + ch * 8)[0] = a0;
+              reinterpret_cast<float4 *>(s_x + (size_t)b * d + ch * 8)[1] = a1;
+            }
+          } else {
+            float(&xq)[8][B] = xr[XS ? 0 : q];
+            xq[0][b] = a0.x; xq[1][b] = a0.y; xq[2][b] = a0.z; xq[3][b] = a0.w;
+            xq[4][b] = a1.x; xq[5][b] = a1.y; xq[6][b] = a1.z; xq[7][b] = a1.w;
+          }
+          const float e8[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) ssl[b] = fmaf(e8[k], e8[k], ssl[b]);
         }
       }
 #pragma unroll
       for (int b = 0; b < B; ++b) {
-        float ss = 0.f;
-#pragma unroll
-        for (int q = 0; q < CH; ++q)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) ss = fmaf(xr[q][k][b], xr[q][k][b], ss);
-        ss = warp_sum(ss);
+        const float ss = warp_sum(ssl[b]);
         if (lane == 0) s_ss[gw][b] = ss;
       }
       if (gt < n_p1) s_b1[gt] = lw.p_b1 ? WT<T>::to_float(lw.p_b1, c + gt * P) : 0.f;
@@ -785,12 +812,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
             const int ch = gt + q * kGroup;
+            float xq_s[XS ? 8 : 1][XS ? B : 1];
+            if constexpr (XS) load_x8<B>(s_x, d, ch, ch < chunks, xq_s);
+            auto &XQ = pick<XS>(xq_s, xr[XS ? 0 : q]);
             float wf[8];
             WT<T>::unpack(lds128z(buf, (size_t)k * row_p1 + (size_t)ch * 16, k < kn && ch < chunks), wf);
 #pragma unroll
             for (int b = 0; b < B; ++b)
 #pragma unroll
-              for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], xr[q][e][b], acc[k * B + b]);
+              for (int e = 0; e < 8; ++e) acc[k * B + b] = fmaf(wf[e], XQ[e][b], acc[k * B + b]);
           }
         }
         float *rb = red + (st & 1) * kGroupWarps * kRedStride;
@@ -845,6 +875,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
 #pragma unroll
             for (int q = 0; q < CH; ++q) {
               const int ch = gt + q * kGroup;
+              float xq_s[XS ? 8 : 1][XS ? B : 1];
+              if constexpr (XS) load_x8<B>(s_x, d, ch, ch < chunks, xq_s);
+              auto &XQ = pick<XS>(xq_s, xr[XS ? 0 : q]);
               const bool ok = g < kn && ch < chunks;
               float wu[8];
               if (REGLU) {
@@ -855,7 +888,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
                 for (int b = 0; b < B; ++b)
 #pragma unroll
                   for (int e = 0; e < 8; ++e)
-                    acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+                    acc[(g * B + b) * 2 + 1] = fmaf(wg[e], XQ[e][b], acc[(g * B + b) * 2 + 1]);
               } else {
                 WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
               }
@@ -864,7 +897,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-                  acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+                  acc[ai] = fmaf(wu[e], XQ[e][b], acc[ai]);
                 }
             }
           }
@@ -1149,12 +1182,15 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
 #pragma unroll
             for (int q = 0; q < CH; ++q) {
               const int ch = gt + q * kGroup;
+              float xq_s[XS ? 8 : 1][XS ? B : 1];
+              if constexpr (XS) load_x8<B>(s_x, d, ch, ch < chunks, xq_s);
+              auto &XQ = pick<XS>(xq_s, xr[XS ? 0 : q]);
               const bool ok = g < kn && ch < chunks;
               const size_t cu = go + (REGLU ? row_ffn : 0);
               float fu[8], pu = 0.f;
               q4_unpack8(ok ? lds32(buf + cu + (size_t)ch * 4) : 0x88888888u, fu);
 #pragma unroll
-              for (int e = 0; e < 8; ++e) pu = fmaf(fu[e], xr[q][e][0], pu);
+              for (int e = 0; e < 8; ++e) pu = fmaf(fu[e], XQ[e][0], pu);
               const float su = ok ? lds_half(buf + cu + (size_t)(d >> 1) + (size_t)(ch >> 2) * 2) : 0.f;
               const int ai = REGLU ? g * 2 : g;
               acc[ai] = fmaf(su, pu, acc[ai]);
@@ -1162,7 +1198,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
                 float fg[8], pg = 0.f;
                 q4_unpack8(ok ? lds32(buf + go + (size_t)ch * 4) : 0x88888888u, fg);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) pg = fmaf(fg[e], xr[q][e][0], pg);
+                for (int e = 0; e < 8; ++e) pg = fmaf(fg[e], XQ[e][0], pg);
                 const float sg = ok ? lds_half(buf + go + (size_t)(d >> 1) + (size_t)(ch >> 2) * 2) : 0.f;
                 acc[g * 2 + 1] = fmaf(sg, pg, acc[g * 2 + 1]);
               }
@@ -1172,6 +1208,9 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
 #pragma unroll
           for (int q = 0; q < CH; ++q) {
             const int ch = gt + q * kGroup;
+            float xq_s[XS ? 8 : 1][XS ? B : 1];
+            if constexpr (XS) load_x8<B>(s_x, d, ch, ch < chunks, xq_s);
+            auto &XQ = pick<XS>(xq_s, xr[XS ? 0 : q]);
             const bool ok = g < kn && ch < chunks;
             float wu[8];
             if (REGLU) {
@@ -1182,7 +1221,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
               for (int b = 0; b < B; ++b)
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
-                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], xr[q][e][b], acc[(g * B + b) * 2 + 1]);
+                  acc[(g * B + b) * 2 + 1] = fmaf(wg[e], XQ[e][b], acc[(g * B + b) * 2 + 1]);
             } else {
               WT<T>::unpack(lds128z(buf, go + (size_t)ch * 16, ok), wu);
             }
@@ -1191,7 +1230,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_layer(const FusedParams p0
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const int ai = REGLU ? (g * B + b) * 2 : g * B + b;
-                acc[ai] = fmaf(wu[e], xr[q][e][b], acc[ai]);
+                acc[ai] = fmaf(wu[e], XQ[e][b], acc[ai]);
               }
           }
         }

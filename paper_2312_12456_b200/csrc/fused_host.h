@@ -172,10 +172,12 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const int NT = (3 * mb + 7) / 8;
   // everything but the ring: mbarriers, reduction buffers, h, logits, b2, b_up/ids/bits, phase-4
   // partials, g staging and its B fragments; the ring gets the rest (<= 200 KB)
+  // B = 2 kernels keep x in shared memory ([B][d] fp32, fused.cuh s_x) instead of registers
+  const size_t xs_bytes = mb >= 2 ? (size_t)mb * d * 4 : 0;
   auto extras = [&](int ns) {
     return (size_t)(3 * ns + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 + (size_t)ns * 8 * mb * 4 +
            (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9 + 16 + (size_t)fused_spart(w.P, w.pcap, mb) * 4 +
-           (size_t)mb * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + 64;
+           (size_t)mb * w.kt * 16 * 4 + (size_t)w.kt * NT * 32 * 8 + xs_bytes + 64;
   };
   const size_t cap = 227 * 1024 - 2560;   // static shared memory (speculative tables, barriers) and slack
   w.NS = (int)std::min<size_t>({200 * 1024 / sb, cap / sb, (size_t)kMaxStages});
@@ -185,7 +187,7 @@ inline bool fused_alloc(FusedWork &w, int d, int m, int r, int maxB, int num_sms
   const size_t pre = (size_t)(3 * w.NS + 2) * 8 + (size_t)2 * kGroupWarps * kRedStride * 4 +
                      (size_t)w.NS * 8 * mb * 4 + (size_t)(2 * mb + 1) * w.wcap * 32 * 4 + (size_t)w.idcap * 9;
   w.part_off = (int)(((size_t)w.NS * sb + pre + 15) / 16 * 16);
-  w.smem = w.part_off + fused_spart(w.P, w.pcap, mb) * 4 + mb * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + 64;
+  w.smem = w.part_off + fused_spart(w.P, w.pcap, mb) * 4 + mb * w.kt * 16 * 4 + w.kt * NT * 32 * 8 + (int)xs_bytes + 64;
   const int words = (m + 31) / 32;
   // a grouped workspace repeats every buffer per group with the strides of fused.cuh group_view
   const size_t G = (size_t)groups;
