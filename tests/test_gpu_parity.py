@@ -177,7 +177,7 @@ def test_golden_g6_reglu_g7_batch(env):
 @pytest.mark.parametrize("act,shape", [("relu", (256, 1000, 64)), ("relu", (136, 777, 24)),
                                        ("reglu", (64, 250, 16)), ("reglu", (40, 97, 8))])
 @pytest.mark.parametrize("dtype", ["bf16", "f16"])
-@pytest.mark.parametrize("B", [1, 3, 8])
+@pytest.mark.parametrize("B", [1, 2, 3, 6, 8])
 def test_integer_layers_bitwise(env, act, shape, dtype, B):
     gen, pi = env
     d, m, r = shape
@@ -205,7 +205,7 @@ def test_integer_layers_bitwise(env, act, shape, dtype, B):
 @pytest.mark.parametrize("name,dims", [("c1", (768, 3072, 64)), ("c2", (4096, 2048, 256)),
                                        ("c3", (5120, 1400, 320)), ("c4", (8192, 1024, 512)),
                                        ("c5", (12288, 520, 768))])
-@pytest.mark.parametrize("B", [1, 4])
+@pytest.mark.parametrize("B", [1, 2, 4, 8])
 def test_random_layers(env, name, dims, B):
     gen, pi = env
     cfg = gen.CONFIGS[name]
@@ -399,13 +399,15 @@ def test_error_paths(env):
 # ---------------------------------------------------------------------------
 # full BASELINE sizes, the bench's launch configuration (one layer each; every output checked)
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
-def test_full_size_layers(env, name):
+@pytest.mark.parametrize("name,B", [("c1", 1), ("c2", 1), ("c3", 1), ("c3", 2), ("c3", 4), ("c3", 8), ("c4", 1),
+                                    ("c4", 2), ("c5", 1)])
+def test_full_size_layers(env, name, B):
+    """Full-size layers at the batch sizes the bench lines run (c3: north_star's B = 1-8; B = 2 is
+    the fused kernel with x in shared memory, B = 8 the x-stationary per-step up projection)."""
     gen, pi = env
     cfg = gen.CONFIGS[name]
     w = gen.make_layer(cfg, seed=0, device="cuda")
     flags = pi.PI_FLAG_INPUT_RMSNORM if cfg.rmsnorm else 0
-    B = 8 if name == "c3" else 1
     L = pi.Layer(w, max_batch=B, flags=flags)
     x = gen.tokens(B, cfg.d, seed=1, device="cuda")
     y, gm, ids, n = run_forward(pi, L, x)
