@@ -1,3 +1,4 @@
+# Phase trace of group 0 of a grouped launch (pi_group_run): python scripts/trace_group.py c2 8 18 3  (config, CTAs per group, groups, layers per group)
 import sys, torch, numpy as np, json
 sys.path.insert(0, '.')
 from paper_2312_12456_b200 import gen, pi
