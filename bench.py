@@ -613,12 +613,13 @@ def main():
         kb = bytes_step.sum(axis=1)
         timing_src = "CUDA events around each launch inside the timed loop"
     else:
-        kt, kb = [], []
+        kt, kb, ar = [], [], []
         for k in range(min(args.steps, 10)):
             i = args.warmup + k
             st = stacks[i % copies]
             e0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
             e1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
+            e2 = [torch.cuda.Event(enable_timing=True) for _ in range(n_layers)]
             cur = xs[i]
             bufs = st._bufs(cur)
             for l, L in enumerate(st.layers):
@@ -628,14 +629,34 @@ def main():
                 e1[l].record(stream)
                 if world > 1:
                     dist.all_reduce(dst)
+                e2[l].record(stream)
                 cur = dst
             torch.cuda.synchronize()
             for l in range(n_layers):
                 kt.append(e0[l].elapsed_time(e1[l]) / 1e3)
+                ar.append(e1[l].elapsed_time(e2[l]) / 1e3)
                 kb.append(algorithmic_bytes(metas[l], int(n_host[k, l]), B))
         timing_src = "CUDA events around each layer's launch in a separate 10-step pass"
     launch_s = float(np.mean(kt))
     bytes_launch = float(np.mean(kb))
+    per_rank = None
+    if world > 1:
+        # the per-GPU view: each rank's fused-layer time, its all-reduce time per
+        # layer and the share of the layer's active neurons it owns (the E9 analogue)
+        try:
+            mine = {"rank": rank, "layer_kernel_us": round(launch_s * 1e6, 2),
+                    "allreduce_us_per_layer": round(float(np.mean(ar)) * 1e6, 2),
+                    "local_active": round(float(n_host.mean()), 1),
+                    "local_activity": round(float(n_host.mean() / metas[0].m_local), 4),
+                    "roofline_frac": round(bytes_launch / launch_s / 1e9 / hbm_peak()[0], 4)}
+            allr = [None] * world
+            dist.all_gather_object(allr, mine)
+            tot = sum(r["local_active"] for r in allr)
+            for r in allr:
+                r["active_share"] = round(r["local_active"] / tot, 4) if tot else None
+            per_rank = allr
+        except Exception as e:   # diagnostic only: never costs the bench line
+            per_rank = {"error": repr(e)}
     peak, peak_src = hbm_peak()
     achieved = bytes_launch / launch_s / 1e9
     kname = ("k_layer x%d layers in one persistent launch (pi_stack_run)" % n_layers) if one_launch else \
@@ -708,7 +729,7 @@ def main():
                    "placement": ilp_info or "fixed"}, args=args),
                "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
                               "p99": float(np.percentile(per_step, 99))},
-               "roofline": roofline, "phases_us": phases, "cpu_baseline": cpu, "e2e": e2e,
+               "roofline": roofline, "phases_us": phases, "per_rank": per_rank, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(args.steps * launches_per_step), "clocks": clk}
         print(json.dumps(out), flush=True)
     if world > 1:
