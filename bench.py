@@ -441,6 +441,7 @@ def run_grouped(args, cfg, B, dev):
                            for k in range(args.steps)])
     realised = float(n_host.mean() / meta.m_local)
     peak, peak_src = hbm_peak()
+    l2_bytes = float(torch.cuda.get_device_properties(dev).L2_cache_size)
     launch_s = per_step / 1e3
     achieved = float(bytes_step.mean()) / float(launch_s.mean()) / 1e9
     roofline = {"bound": "hbm", "kernel": "k_layer grouped launch (pi_group_run): %d groups x %d CTAs, %d layer "
@@ -477,8 +478,9 @@ def run_grouped(args, cfg, B, dev):
                            "layer_tokens_per_step": lt,
                            "note": "value = layer-tokens/s: each group decodes its own token through its own "
                                    "chain of distinct layer copies; all groups in one persistent launch"},
-               "l2": "%d distinct layer copies, %.0f MB of algorithmic bytes per step (> L2)" % (
-                   ng * gl, float(bytes_step.mean()) / 1e6),
+               "l2": "%d distinct layer copies, %.0f MB of algorithmic bytes per step (%s the %.0f MB L2)" % (
+                   ng * gl, float(bytes_step.mean()) / 1e6,
+                   "above" if bytes_step.mean() > l2_bytes else "NOT above", l2_bytes / 1e6),
                "algorithmic_MB_per_step": round(float(bytes_step.mean()) / 1e6, 2)}, args=args),
            "latency_ms": {"p50": float(np.percentile(per_step, 50)), "p95": float(np.percentile(per_step, 95)),
                           "p99": float(np.percentile(per_step, 99))},
