@@ -229,9 +229,7 @@ __device__ __forceinline__ void p2_phase(const P2Ctx &x) {
         uint16_t p0[3], p1[3];
         Split3<T>::split(gv[q][2 * h] * s_b, p0);
         Split3<T>::split(gv[q][2 * h + 1] * s_b, p1);
-        const uint16_t a = s == 0 ? p0[0] : (s == 1 ? p0[1] : p0[2]);   // no dynamic register-array index
-        const uint16_t c2 = s == 0 ? p1[0] : (s == 1 ? p1[1] : p1[2]);
-        r2[h] = (uint32_t)a | ((uint32_t)c2 << 16);
+        r2[h] = (uint32_t)p0[s] | ((uint32_t)p1[s] << 16);
       }
       x.gfrag[K * 32 + L] = make_uint2(r2[0], r2[1]);
     }
